@@ -1,0 +1,174 @@
+// common.cuh -- shared host/device helpers for the polynewt_b200 kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <type_traits>
+
+#include "../../include/polynewt_b200.h"
+#include "xprec.cuh"
+
+namespace pn {
+
+// ---------------------------------------------------------------------------
+// host error plumbing: every C-ABI entry point returns a status and leaves a
+// message in a thread-local buffer (pn_last_error)
+
+void set_error(const char *fmt, ...);
+
+struct Fail {
+  int code;
+};
+
+#define PN_CHECK_CUDA(expr)                                                            \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ::pn::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__,  \
+                      __LINE__, cudaGetErrorString(_e));                               \
+      throw ::pn::Fail{PN_E_CUDA};                                                     \
+    }                                                                                  \
+  } while (0)
+
+#define PN_CHECK_LAUNCH() PN_CHECK_CUDA(cudaGetLastError())
+
+#define PN_REQUIRE(cond, code, ...)        \
+  do {                                     \
+    if (!(cond)) {                         \
+      ::pn::set_error(__VA_ARGS__);        \
+      throw ::pn::Fail{code};              \
+    }                                      \
+  } while (0)
+
+// convert exceptions to status codes at the C boundary
+#define PN_API_BEGIN try {
+#define PN_API_END                                             \
+  }                                                            \
+  catch (const ::pn::Fail &f) {                                \
+    return f.code;                                             \
+  }                                                            \
+  catch (const std::bad_alloc &) {                             \
+    ::pn::set_error("host allocation failed");                 \
+    return PN_E_NOMEM;                                         \
+  }                                                            \
+  catch (...) {                                                \
+    ::pn::set_error("unexpected C++ exception");               \
+    return PN_E_CUDA;                                          \
+  }                                                            \
+  return PN_OK;
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// kernel-launch bookkeeping: bench.py reports how many of our kernels ran
+void count_launch(int n = 1);
+
+// ---------------------------------------------------------------------------
+// device: canonical pairwise tree reduction over per-thread partials.
+//
+// tree_sum (varith.py:169-191) pairs (0,1),(2,3),... level by level and
+// carries an odd tail; that equals stride-doubling: at stride s, index t
+// (a multiple of 2s) absorbs t+s when t+s < n.  Thread t holds
+// the partial of the aligned block t; nparts = number of blocks.  The result
+// is returned in every thread.  sm must hold NT/32 elements.
+template <class E, int NT>
+__device__ __forceinline__ E block_tree_reduce(E v, int nparts, E *sm) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    E o = eshfl_down(v, s);
+    if ((lane & (2 * s - 1)) == 0 && t + s < nparts) v = eadd(v, o);
+  }
+  constexpr int NW = NT / 32;
+  if constexpr (NW > 1) {
+    if (lane == 0) sm[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      const int nw = (nparts + 31) / 32;
+      E x = (lane < NW) ? sm[lane] : sm[0];
+#pragma unroll
+      for (int s = 1; s < NW; s <<= 1) {
+        E o = eshfl_down(x, s);
+        if ((lane & (2 * s - 1)) == 0 && lane + s < nw) x = eadd(x, o);
+      }
+      if (lane == 0) sm[0] = x;
+    }
+    __syncthreads();
+    v = sm[0];
+    __syncthreads();
+  } else {
+    const double *s = reinterpret_cast<const double *>(&v);
+    E r;
+    double *d = reinterpret_cast<double *>(&r);
+#pragma unroll
+    for (int i = 0; i < Traits<E>::es; ++i) d[i] = __shfl_sync(0xffffffffu, s[i], 0);
+    v = r;
+  }
+  return v;
+}
+
+// sequential pairwise tree over a register array of B elements where only
+// the first `valid` are present (aligned block; right-pruned)
+template <class E, int B>
+__device__ __forceinline__ E local_tree(E (&v)[B], int valid) {
+#pragma unroll
+  for (int s = 1; s < B; s <<= 1) {
+#pragma unroll
+    for (int t = 0; t + s < B; t += 2 * s) {
+      if (t + s < valid) v[t] = eadd(v[t], v[t + s]);
+    }
+  }
+  return v[0];
+}
+
+// element load/store on component planes: plane p of a (cshape, count)
+// array lives at base + p*count
+template <class E>
+__device__ __forceinline__ E eload_planes(const double *__restrict__ base, long long count, long long i) {
+  E r;
+  double *d = reinterpret_cast<double *>(&r);
+#pragma unroll
+  for (int p = 0; p < Traits<E>::es; ++p) d[p] = base[p * count + i];
+  return r;
+}
+template <class E>
+__device__ __forceinline__ void estore_planes(double *__restrict__ base, long long count, long long i, const E &v) {
+  const double *d = reinterpret_cast<const double *>(&v);
+#pragma unroll
+  for (int p = 0; p < Traits<E>::es; ++p) base[p * count + i] = d[p];
+}
+
+// level dispatch: calls f.template operator()<E>() for the level's element type
+template <class Fn>
+inline void dispatch_level(int nc, int cplx, Fn &&f) {
+  if (cplx) {
+    if (nc == 1) f.template operator()<C<1>>();
+    else if (nc == 2) f.template operator()<C<2>>();
+    else f.template operator()<C<4>>();
+  } else {
+    if (nc == 1) f.template operator()<F<1>>();
+    else if (nc == 2) f.template operator()<F<2>>();
+    else f.template operator()<F<4>>();
+  }
+}
+
+inline void check_level(int nc, int cplx) {
+  PN_REQUIRE((nc == 1 || nc == 2 || nc == 4) && (cplx == 0 || cplx == 1), PN_E_ARG,
+             "precision level must have nc in {1,2,4} and cplx in {0,1} (got nc=%d cplx=%d)", nc, cplx);
+}
+
+#ifdef PN_NC
+// the precision level compiled by this translation unit
+using PnLevel = std::conditional_t<PN_CPLX, C<PN_NC>, F<PN_NC>>;
+#endif
+
+}  // namespace pn

@@ -1,0 +1,434 @@
+// evaldiff.cu -- subsystems (1)+(2): monomial evaluation with reverse-mode
+// differentiation on binary product trees, and the fixed-order accumulation
+// of values and Jacobian entries.
+//
+// Reference: evaluate_system (evaldiff.py:215-266), eval_monomial_and_derivs
+// (142-180), eval_product_tree (53-73), gradient_from_tree (76-108),
+// _tree_reduce (205-212), build_power_table / eval_common_factor
+// (polyrep.py:120-139).
+//
+// Kernels
+//   K0 k_power_table : x_v^d for d = 1..maxdeg_v (one thread per variable)
+//   K1 k_mono_small  : k <= 1 monomials (constant, single-variable bypass)
+//   K1 k_mono_tree   : 2 <= k <= 32; a group of G lanes per monomial.  Lane
+//                      r owns tree nodes t == r (mod G): the low levels of
+//                      the sequential-addressing tree are lane-local, the top
+//                      log2(G) levels are butterflies over warp shuffles
+//                      (every lane computes its node redundantly, so no lane
+//                      idles and the downward sweep needs one shuffle per
+//                      level).  Operand order is the reference's (lower index
+//                      on the left), so results are bit-identical.
+//   K1 k_mono_large  : k > 32 (e.g. cyclic n-roots): one CTA per monomial,
+//                      tree levels in shared memory (the paper's scheme)
+//   K2 k_segments    : one thread per output entry; a binary-counter fold of
+//                      the entry's contributions reproduces tree_sum's
+//                      right-pruned pairwise order exactly.
+#include "common.cuh"
+#include "internal.h"
+
+namespace pn {
+
+// ---------------------------------------------------------------------------
+// K0
+
+template <class E>
+__global__ void k_power_table(int n, const double *__restrict__ x, const int32_t *__restrict__ toff,
+                              const int32_t *__restrict__ tdeg, double *__restrict__ table) {
+  constexpr int es = Traits<E>::es;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int deg = tdeg[v];
+  if (deg == 0) return;
+  const E xv = eload<E>(x + (long long)v * es);
+  double *row = table + (long long)toff[v] * es;
+  E cur = xv;
+  estore(row, cur);
+  for (int d = 2; d <= deg; ++d) {
+    cur = emul(cur, xv);  // row[d] = row[d-1] * x (polyrep.py:128)
+    estore(row + (long long)(d - 1) * es, cur);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1, k <= 1
+
+template <class E>
+__global__ void k_mono_small(const int32_t *__restrict__ list, long long count, const int32_t *__restrict__ mon_ptr,
+                             const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                             const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                             const double *__restrict__ table, const int32_t *__restrict__ toff,
+                             double *__restrict__ contrib) {
+  constexpr int es = Traits<E>::es;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < count;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int c = list[g];
+    const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
+    const E co = eload<E>(coeff + (long long)c * es);
+    if (k == 0) {  // evaldiff.py:152-153
+      estore(contrib + (long long)c * es, co);
+      continue;
+    }
+    // single-variable bypass, evaldiff.py:156-165
+    const int v = var[lo], d = exps[lo];
+    const double *row = table + (long long)toff[v] * es;
+    const E value = emul(co, eload<E>(row + (long long)(d - 1) * es));
+    const E dco = emul_int(co, d);
+    const E deriv = (d == 1) ? dco : emul(dco, eload<E>(row + (long long)(d - 2) * es));
+    estore(contrib + (long long)c * es, value);
+    estore(contrib + (long long)dst[lo] * es, deriv);
+  }
+}
+
+// scale = coeff [* common]; common = left fold of x_v^(d-1) over d >= 2
+// (polyrep.py:133-139, evaldiff.py:168)
+template <class E>
+__device__ __forceinline__ E monomial_scale(const E &co, int lo, int k, const int32_t *__restrict__ var,
+                                            const int32_t *__restrict__ exps, const double *__restrict__ table,
+                                            const int32_t *__restrict__ toff) {
+  constexpr int es = Traits<E>::es;
+  bool have = false;
+  E common;
+  for (int p = 0; p < k; ++p) {
+    const int d = exps[lo + p];
+    if (d < 2) continue;
+    const E pw = eload<E>(table + ((long long)toff[var[lo + p]] + d - 2) * es);
+    common = have ? emul(common, pw) : pw;
+    have = true;
+  }
+  return have ? emul(co, common) : co;
+}
+
+// ---------------------------------------------------------------------------
+// K1, 2 <= k <= 32: G lanes per monomial, BASE = 2^floor(log2 k)
+
+template <int V> struct Log2 { static constexpr int value = 1 + Log2<V / 2>::value; };
+template <> struct Log2<1> { static constexpr int value = 0; };
+
+template <class E, int BASE, int G, int NT>
+__global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ list, long long count,
+                                                  const int32_t *__restrict__ mon_ptr,
+                                                  const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                                                  const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                                                  const double *__restrict__ x, const double *__restrict__ table,
+                                                  const int32_t *__restrict__ toff, double *__restrict__ contrib) {
+  constexpr int es = Traits<E>::es;
+  constexpr int SL = BASE / G;            // slots per lane
+  constexpr int NLOC = Log2<SL>::value;   // lane-local levels above the slots
+  constexpr int NX = Log2<G>::value;      // butterfly levels
+  constexpr int NLV = SL > 1 ? SL - 1 : 1;
+  static_assert(BASE >= G && G >= 2 && G <= 32, "bad tree config");
+
+  const long long grp = (blockIdx.x * (long long)NT + threadIdx.x) / G;
+  const int r = threadIdx.x % G;
+  const bool active = grp < count;
+  const int c = list[active ? grp : count - 1];
+  const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
+  const int ell = k - BASE;
+  const int32_t *__restrict__ mv = var + lo;
+
+  auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
+  // slot t of level 0: v[t] * v[BASE+t] for t < ell, else v[t] (evaldiff.py:63-65)
+  auto slot = [&](int t) -> E {
+    E v = leaf(t);
+    if (t < ell) v = emul(v, leaf(BASE + t));
+    return v;
+  };
+
+  // ---- upward sweep (evaldiff.py:67-72) --------------------------------
+  // lv holds lane-local levels 1..NLOC; level j has SL>>j entries at
+  // offset SL - (SL >> (j-1)); entry u is global node r + G*u.
+  E lv[NLV];
+  E X[NX + 1];
+  if constexpr (NLOC == 0) {
+    X[0] = slot(r);
+  } else {
+#pragma unroll
+    for (int u = 0; u < SL / 2; ++u) lv[u] = emul(slot(r + G * u), slot(r + G * (u + SL / 2)));
+#pragma unroll
+    for (int j = 2; j <= NLOC; ++j) {
+      const int oprev = SL - (SL >> (j - 2)), ocur = SL - (SL >> (j - 1)), h = SL >> j;
+#pragma unroll
+      for (int u = 0; u < h; ++u) lv[ocur + u] = emul(lv[oprev + u], lv[oprev + u + h]);
+    }
+    X[0] = lv[SL - 2];
+  }
+  // butterflies: level of size S = G >> q; lane r holds node r mod S
+#pragma unroll
+  for (int q = 1; q <= NX; ++q) {
+    const int S = G >> q;
+    const E other = eshfl_xor(X[q - 1], S);
+    const bool low = (r & (2 * S - 1)) < S;  // lower index stays the left operand
+    X[q] = emul(low ? X[q - 1] : other, low ? other : X[q - 1]);
+  }
+  const E root = X[NX];
+
+  // ---- value (evaldiff.py:166-172) ---------------------------------------
+  const E co = eload<E>(coeff + (long long)c * es);
+  const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
+  if (active && r == 0) estore(contrib + (long long)c * es, emul(scale, root));
+
+  // ---- downward sweep of complements (evaldiff.py:89-98) -----------------
+  // complement of this lane's node at the current level
+  E cmp = eshfl_xor(X[NX - 1], 1);  // comp = [L[1], L[0]] at the size-2 level
+#pragma unroll
+  for (int q = NX - 2; q >= 0; --q) {
+    const int S = G >> (q + 1);
+    cmp = emul(cmp, eshfl_xor(X[q], S));
+  }
+  // lane-local levels: comp_{j-1}[u] = comp_j[u] * L_{j-1}[u+h],
+  //                    comp_{j-1}[u+h] = comp_j[u] * L_{j-1}[u]
+  E cl[SL];
+  if constexpr (NLOC == 0) {
+    cl[0] = cmp;
+  } else {
+    lv[SL - 2] = cmp;  // complement of the level-NLOC node (size G)
+#pragma unroll
+    for (int j = NLOC; j >= 2; --j) {
+      const int ocur = SL - (SL >> (j - 1)), oprev = SL - (SL >> (j - 2)), h = SL >> j;
+#pragma unroll
+      for (int u = 0; u < h; ++u) {
+        const E cu = lv[ocur + u];
+        const E lo_ = emul(cu, lv[oprev + u + h]);
+        const E hi_ = emul(cu, lv[oprev + u]);
+        lv[oprev + u] = lo_;
+        lv[oprev + u + h] = hi_;
+      }
+    }
+    // level 1 -> slots
+#pragma unroll
+    for (int u = 0; u < SL / 2; ++u) {
+      const E cu = lv[u];
+      cl[u] = emul(cu, slot(r + G * (u + SL / 2)));
+      cl[u + SL / 2] = emul(cu, slot(r + G * u));
+    }
+  }
+
+  // ---- unfold folded pairs and scale (evaldiff.py:100-108, 174-180) -------
+  if (!active) return;
+#pragma unroll
+  for (int u = 0; u < SL; ++u) {
+    const int t = r + G * u;
+    if (t < ell) {
+      const int t2 = BASE + t;
+      const E g1 = emul(cl[u], leaf(t2));
+      const E g2 = emul(cl[u], leaf(t));
+      const int d1 = exps[lo + t], d2 = exps[lo + t2];
+      const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
+      const E s2 = d2 == 1 ? scale : emul_int(scale, d2);
+      estore(contrib + (long long)dst[lo + t] * es, emul(s1, g1));
+      estore(contrib + (long long)dst[lo + t2] * es, emul(s2, g2));
+    } else {
+      const int d1 = exps[lo + t];
+      const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
+      estore(contrib + (long long)dst[lo + t] * es, emul(s1, cl[u]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1, k > 32: one CTA per monomial, tree levels in shared memory
+
+template <class E, int NT>
+__global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ list, long long count,
+                                                   const int32_t *__restrict__ mon_ptr,
+                                                   const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                                                   const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                                                   const double *__restrict__ x, const double *__restrict__ table,
+                                                   const int32_t *__restrict__ toff, double *__restrict__ contrib) {
+  constexpr int es = Traits<E>::es;
+  extern __shared__ __align__(16) double smem[];
+  E *lvl = reinterpret_cast<E *>(smem);  // levels back to back: 2*BASE entries
+  __shared__ E s_scale;
+  for (long long g = blockIdx.x; g < count; g += gridDim.x) {
+    const int c = list[g];
+    const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
+    int base = 1;
+    while (base * 2 <= k) base *= 2;
+    const int ell = k - base;
+    const int32_t *__restrict__ mv = var + lo;
+    auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
+    for (int t = threadIdx.x; t < base; t += NT) {
+      E v = leaf(t);
+      if (t < ell) v = emul(v, leaf(base + t));
+      lvl[t] = v;
+    }
+    __syncthreads();
+    // level offsets: level j starts at 2*base - (2*base >> j)
+    int off = 0;
+    for (int size = base; size > 1; size >>= 1) {
+      const int s = size / 2;
+      for (int t = threadIdx.x; t < s; t += NT) lvl[off + size + t] = emul(lvl[off + t], lvl[off + t + s]);
+      off += size;
+      __syncthreads();
+    }
+    const E root = lvl[off];
+    if (threadIdx.x == 0) {
+      const E co = eload<E>(coeff + (long long)c * es);
+      const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
+      s_scale = scale;
+      estore(contrib + (long long)c * es, emul(scale, root));
+    }
+    // complements, in place over a separate buffer of base entries
+    E *cmp = lvl + 2 * base;
+    // size-2 level starts at off - 2
+    if (threadIdx.x == 0) {
+      cmp[0] = lvl[off - 2 + 1];
+      cmp[1] = lvl[off - 2];
+    }
+    __syncthreads();
+    int o2 = off - 2;  // offset of the size-2 level
+    for (int s = 2; s < base; s <<= 1) {
+      const int oprev = o2 - 2 * s;  // level of size 2s
+      for (int t = threadIdx.x; t < s; t += NT) {
+        const E ct = cmp[t];
+        const E a = emul(ct, lvl[oprev + t + s]);
+        const E b = emul(ct, lvl[oprev + t]);
+        cmp[t] = a;
+        cmp[t + s] = b;
+      }
+      o2 = oprev;
+      __syncthreads();
+    }
+    const E scale = s_scale;
+    for (int t = threadIdx.x; t < base; t += NT) {
+      if (t < ell) {
+        const int t2 = base + t;
+        const E g1 = emul(cmp[t], leaf(t2));
+        const E g2 = emul(cmp[t], leaf(t));
+        const int d1 = exps[lo + t], d2 = exps[lo + t2];
+        estore(contrib + (long long)dst[lo + t] * es, emul(d1 == 1 ? scale : emul_int(scale, d1), g1));
+        estore(contrib + (long long)dst[lo + t2] * es, emul(d2 == 1 ? scale : emul_int(scale, d2), g2));
+      } else {
+        const int d1 = exps[lo + t];
+        estore(contrib + (long long)dst[lo + t] * es, emul(d1 == 1 ? scale : emul_int(scale, d1), cmp[t]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: one thread per output entry
+
+template <class E>
+__global__ void __launch_bounds__(128) k_segments(long long nseg_total, int m, const int64_t *__restrict__ seg_ptr,
+                                                  const int64_t *__restrict__ seg_out,
+                                                  const double *__restrict__ contrib, double *__restrict__ f,
+                                                  double *__restrict__ A, long long negf_off) {
+  constexpr int es = Traits<E>::es;
+  E stk[32];
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg_total;
+       s += (long long)gridDim.x * blockDim.x) {
+    const long long a = seg_ptr[s], b = seg_ptr[s + 1];
+    const long long L = b - a;
+    E acc;
+    if (L == 0) {
+      acc = ezero<E>();  // zero_like(point[0]) for an empty polynomial (evaldiff.py:261)
+    } else {
+      for (long long p = 0; p < L; ++p) {
+        E carry = eload<E>(contrib + (a + p) * es);
+        int lvl = 0;
+        for (long long q = p; q & 1; q >>= 1, ++lvl) carry = eadd(stk[lvl], carry);
+        stk[lvl] = carry;
+      }
+      int l = __ffsll(L) - 1;
+      acc = stk[l];
+      for (++l; l < 32; ++l)
+        if ((L >> l) & 1) acc = eadd(stk[l], acc);
+    }
+    if (s < m) {
+      if (f) estore(f + s * es, acc);
+      if (negf_off >= 0) estore(A + (negf_off + s) * es, eneg(acc));
+    } else {
+      estore(A + seg_out[s - m] * es, acc);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+template <class E> struct TreeG;  // lanes per monomial, by precision
+template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
+template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
+
+template <class E, int BASE>
+static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double *x, double *contrib,
+                        cudaStream_t st) {
+  constexpr int G = TreeG<E>::value < BASE ? TreeG<E>::value : BASE;
+  constexpr int NT = 128;
+  const long long threads = b.count * G;
+  const int grid = (int)((threads + NT - 1) / NT);
+  k_mono_tree<E, BASE, G, NT><<<grid, NT, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,
+                                                   sys->d_dst, sys->d_coeff, x, sys->table.d(), sys->d_toff,
+                                                   contrib);
+  PN_CHECK_LAUNCH();
+  count_launch(1);
+}
+
+template <class E>
+void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
+                          cudaStream_t st) {
+  constexpr int es = Traits<E>::es;
+  const long long M = sys->M, nnz = sys->nnz;
+  PN_REQUIRE(ldA == sys->m, PN_E_ARG, "internal: Jacobian leading dimension must equal m");
+  sys->contrib.ensure((size_t)(M + nnz) * es * sizeof(double) + 16);
+  sys->table.ensure((size_t)(sys->table_len > 0 ? sys->table_len : 1) * es * sizeof(double));
+  double *contrib = sys->contrib.d();
+  if (sys->table_len > 0) {
+    k_power_table<E><<<(sys->n + 127) / 128, 128, 0, st>>>(sys->n, x, sys->d_toff, sys->d_tdeg, sys->table.d());
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+  }
+  for (const auto &b : sys->buckets) {
+    if (b.count == 0) continue;
+    if (b.kind == 0) {
+      const int grid = (int)std::min<long long>((b.count + 127) / 128, (long long)num_sms() * 16);
+      k_mono_small<E><<<grid, 128, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp, sys->d_dst,
+                                            sys->d_coeff, sys->table.d(), sys->d_toff, contrib);
+      PN_CHECK_LAUNCH();
+      count_launch(1);
+    } else if (b.kind == 1) {
+      switch (b.base) {
+        case 2: launch_tree<E, 2>(b, sys, x, contrib, st); break;
+        case 4: launch_tree<E, 4>(b, sys, x, contrib, st); break;
+        case 8: launch_tree<E, 8>(b, sys, x, contrib, st); break;
+        case 16: launch_tree<E, 16>(b, sys, x, contrib, st); break;
+        case 32: launch_tree<E, 32>(b, sys, x, contrib, st); break;
+        default: PN_REQUIRE(false, PN_E_ARG, "internal: bad bucket base %d", b.base);
+      }
+    } else {
+      int base = 1;
+      while (base * 2 <= sys->max_k) base *= 2;
+      const size_t smem = (size_t)3 * base * es * sizeof(double);
+      PN_REQUIRE(smem <= 227 * 1024, PN_E_ARG,
+                 "monomials with %d variables exceed the shared-memory tree capacity", sys->max_k);
+      constexpr int NT = 256;
+      PN_CHECK_CUDA(cudaFuncSetAttribute(k_mono_large<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      const int grid = (int)std::min<long long>(b.count, (long long)num_sms() * 8);
+      k_mono_large<E, NT><<<grid, NT, smem, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,
+                                                  sys->d_dst, sys->d_coeff, x, sys->table.d(), sys->d_toff, contrib);
+      PN_CHECK_LAUNCH();
+      count_launch(1);
+    }
+  }
+  // dense Jacobian: absent entries are exact zeros (evaldiff.py:262)
+  PN_CHECK_CUDA(cudaMemsetAsync(A, 0, (size_t)sys->n * ldA * es * sizeof(double), st));
+  const long long total = sys->m + sys->nseg;
+  if (total > 0) {
+    const int grid = (int)std::min<long long>((total + 127) / 128, (long long)num_sms() * 32);
+    k_segments<E><<<grid, 128, 0, st>>>(total, sys->m, sys->d_seg_ptr, sys->d_seg_out, contrib, f, A,
+                                        negf_col >= 0 ? (long long)negf_col * ldA : -1);
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+  }
+}
+
+// one translation unit per precision level (see Makefile): explicit
+// instantiation for the level selected by PN_NC / PN_CPLX
+#ifdef PN_NC
+template void evaldiff_impl<PnLevel>(pn_system *, const double *, double *, double *, long long, int,
+                                      cudaStream_t);
+#endif
+
+}  // namespace pn

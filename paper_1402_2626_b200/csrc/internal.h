@@ -1,0 +1,186 @@
+// internal.h -- declarations shared by the translation units of
+// libpolynewt_b200.so (not part of the public C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/polynewt_b200.h"
+
+namespace pn {
+
+void set_error(const char *fmt, ...);
+void count_launch(int n);
+
+// ---------------------------------------------------------------------------
+// device memory helpers
+
+bool is_device_ptr(const void *p);
+
+// stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync)
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t nbytes, cudaStream_t st);
+  ~DevBuf();
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  DevBuf(DevBuf &&o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; }
+  DevBuf &operator=(DevBuf &&o) noexcept {
+    if (this != &o) {
+      if (p) cudaFreeAsync(p, s);
+      p = o.p;
+      bytes = o.bytes;
+      s = o.s;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  double *d() const { return static_cast<double *>(p); }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// persistent device allocation (cudaMalloc), grown on demand
+struct DevArena {
+  void *p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t nbytes);
+  ~DevArena();
+  double *d() const { return static_cast<double *>(p); }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+// read-only input on the device: either the caller's device pointer or a
+// staged copy of a host buffer
+struct DevIn {
+  const double *d = nullptr;
+  DevBuf own;
+  DevIn(const double *src, size_t ndoubles, cudaStream_t st);
+};
+
+// output: device pointer of the caller or a scratch buffer copied back by finish()
+struct DevOut {
+  double *d = nullptr;
+  double *host = nullptr;
+  size_t n = 0;
+  DevBuf own;
+  DevOut(double *dst, size_t ndoubles, cudaStream_t st);
+  void finish(cudaStream_t st);  // enqueue D2H copy if host
+};
+
+// ---------------------------------------------------------------------------
+// layout conversion (component planes <-> AoS elements)
+
+// planes (es, rows, cols) row-major  ->  AoS column-major with leading dim ld
+void planes_to_aos_colmajor(int es, int rows, int cols, const double *src, double *dst, long long ld,
+                            cudaStream_t st);
+// AoS column-major (ld)  ->  planes (es, rows, cols) row-major
+void aos_colmajor_to_planes(int es, int rows, int cols, const double *src, long long ld, double *dst,
+                            cudaStream_t st);
+// 1-D: planes (es, n) <-> AoS (n, es)
+void planes_to_aos(int es, long long n, const double *src, double *dst, cudaStream_t st);
+void aos_to_planes(int es, long long n, const double *src, double *dst, cudaStream_t st);
+
+// element-wise op on AoS arrays (used inside the Newton step)
+void vec_op_aos(int nc, int cplx, int op, long long n, const double *a, const double *b, double *out,
+                cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// MGS least squares on a device-resident augmented matrix
+//   A : AoS column-major (m rows, n+1 cols, ld = m), overwritten
+//   Q : AoS column-major (m, n) or NULL
+//   R : AoS column-major ((n+1) x (n+1), ld = n+1), zero-initialised here
+// status (device int[4]) + info (device double[4]) receive the breakdown
+// record; the call enqueues work on st and returns without synchronising.
+constexpr int kMgsThreads = 256;     // CTA size of the MGS sweeps
+constexpr int kBacksubThreads = 256;  // CTA size of back substitution (n <= 4 * this)
+inline int rows_per_thread(int m) {
+  int per = (m + kMgsThreads - 1) / kMgsThreads, B = 1;
+  while (B < per) B <<= 1;
+  return B;
+}
+struct MgsStatus {
+  int code;  // 0 ok, PN_E_BREAKDOWN, PN_E_SINGULAR
+  int k;
+  double rkk, thr;
+};
+struct MgsWork {
+  DevArena qbuf;    // normalized pivot columns when Q is not requested
+  DevArena orig;    // orig column norms (hi)
+  DevArena status;  // int32[4] + double[4]
+};
+void mgs_factor_device(int nc, int cplx, int m, int n, double *A, double *Q, double *R, MgsWork &w,
+                       cudaStream_t st);
+// back substitution on the device-resident R (column-major, ld = n+1); x AoS
+void backsub_device(int nc, int cplx, int n, const double *R, double *x, MgsWork &w, cudaStream_t st);
+// read the status record written by mgs/backsub; returns PN_OK / PN_E_BREAKDOWN / PN_E_SINGULAR
+int mgs_read_status(MgsWork &w, pn_numinfo *info, cudaStream_t st);
+
+}  // namespace pn
+
+// ---------------------------------------------------------------------------
+// the packed, device-resident system (evaldiff.py:183-194 PreparedSystem)
+struct pn_system {
+  int nc = 0, cplx = 0, es = 0;
+  int m = 0, n = 0;
+  long long M = 0, nnz = 0;
+  long long nseg = 0;  // Jacobian segments (nonzero entries)
+  int max_k = 0, max_deg = 0;
+  std::vector<long long> perm;  // canonical position -> input monomial
+  pn_counts counts{};
+  pn_system_stats stats{};
+
+  // device arrays (canonical order)
+  int32_t *d_mon_ptr = nullptr;  // M+1
+  int32_t *d_var = nullptr;      // nnz
+  int32_t *d_exp = nullptr;      // nnz
+  int32_t *d_dst = nullptr;      // nnz: contribution slot of each support entry
+  double *d_coeff = nullptr;     // M * es (AoS)
+  int32_t *d_toff = nullptr;     // n: power-table row offset per variable
+  int32_t *d_tdeg = nullptr;     // n: max exponent per variable (0 = absent)
+  int64_t *d_seg_ptr = nullptr;  // m + nseg + 1 segment starts in the contribution buffer
+  int64_t *d_seg_out = nullptr;  // nseg: output index (column-major j*m + i) of J segments
+  long long table_len = 0;
+
+  // monomial buckets by kind, device lists of canonical monomial indices
+  struct Bucket {
+    int kind;        // 0: k<=1, 1: tree with BASE=base, 2: large tree
+    int base;
+    long long count;
+    int32_t *d_list;
+  };
+  std::vector<Bucket> buckets;
+
+  // scratch reused across evaluations
+  pn::DevArena contrib;  // (M + nnz) * es
+  pn::DevArena table;    // table_len * es
+  pn::DevArena xbuf;     // n * es
+  pn::DevArena Abuf;     // m * (n+1) * es (Newton / evaldiff output)
+  pn::DevArena Rbuf, xsol, fbuf, vbuf;
+  pn::MgsWork mgs;
+  cudaEvent_t ev = nullptr;
+
+  ~pn_system();
+};
+
+namespace pn {
+// evaluate at x (AoS, device) into f (AoS, device, may be NULL) and the
+// Jacobian, written column-major with leading dimension ldA into A (zeroed
+// entries included).  If negf_col >= 0, -f is additionally written into
+// column negf_col of A (the b column of [J -f]).
+void evaldiff_device(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
+                     cudaStream_t st);
+
+// per-level implementations (explicitly instantiated in one TU per level)
+template <class E>
+void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
+                   cudaStream_t st);
+template <class E>
+void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st);
+template <class E>
+void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st);
+}  // namespace pn

@@ -1,0 +1,131 @@
+"""Benchmark systems and seeded inputs (mirror of polynewt.bench, plus the
+SURVEY 8(d) random sparse family F(n, T, k) generated natively).
+
+Inputs are produced on the host once and shipped as component planes; the
+points use Python's ``random.Random`` exactly like the reference
+(bench.py:72-95), so both paths see identical values.
+"""
+
+from __future__ import annotations
+
+import math
+import random
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from .polyrep import Monomial, PackedSystem, PolySystem
+from .xprec import PrecisionLevel
+
+
+def random_sparse_system(n: int, T: int, k: int, level: PrecisionLevel, seed: int, maxexp: int = 1,
+                         m: int | None = None) -> PackedSystem:
+    """F(n, T, k, level, seed, maxexp, m): m polynomials of T monomials, each
+    a product of k distinct variables with exponents in [1, maxexp] and
+    coefficient parts in +-[0.5, 2).  Built by the C ABI's
+    splitmix64 generator in generation order (not canonical)."""
+    m = n if m is None else m
+    M = m * T
+    nnz = M * k
+    poly_ptr = np.empty(m + 1, np.int32)
+    mon_ptr = np.empty(M + 1, np.int32)
+    var_idx = np.empty(nnz, np.int32)
+    exps = np.empty(nnz, np.int32)
+    re = np.empty(M)
+    im = np.empty(M) if level.cplx else None
+    rc = _lib.load().pn_generate_random_system(m, n, T, k, maxexp, seed, _lib.ptr(poly_ptr), _lib.ptr(mon_ptr),
+                                               _lib.ptr(var_idx), _lib.ptr(exps), _lib.ptr(re), _lib.ptr(im))
+    _lib.check(rc)
+    coeffs = np.zeros(level.cshape + (M,))
+    # level.from_float(v): DoubleDouble(v) = (v + 0.0, 0.0); QuadDouble alike
+    if level.cplx:
+        coeffs[0, 0] = re + 0.0
+        coeffs[1, 0] = im + 0.0
+    else:
+        coeffs[0] = re + 0.0
+    return PackedSystem(level, n, poly_ptr, mon_ptr, var_idx, exps, coeffs)
+
+
+def random_point(n: int, seed: int, level: PrecisionLevel) -> list:
+    """n random values with magnitudes in [0.5, 2) (bench.py:84-95)."""
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        re = rng.uniform(0.5, 2.0) * rng.choice((-1.0, 1.0))
+        if level.cplx:
+            out.append(level.from_float(re, rng.uniform(0.5, 2.0) * rng.choice((-1.0, 1.0))))
+        else:
+            out.append(level.from_float(re))
+    return out
+
+
+def random_unit_point(n: int, seed: int, level: PrecisionLevel) -> list:
+    """n random unit-modulus complex values (bench.py:72-81)."""
+    if not level.cplx:
+        raise ValueError("unit-circle points need a complex level")
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        theta = rng.uniform(0.0, 2.0 * math.pi)
+        out.append(level.from_float(math.cos(theta), math.sin(theta)))
+    return out
+
+
+def cyclic_n_roots(n: int, level: PrecisionLevel) -> PolySystem:
+    """Cyclic n-roots system (bench.py:51-69)."""
+    if n < 2:
+        raise ValueError("need n >= 2")
+    one = level.one()
+    polys = []
+    for i in range(1, n):
+        terms = []
+        for j in range(n):
+            vars_ = sorted((j + k) % n for k in range(i))
+            terms.append(Monomial(one, tuple((v, 1) for v in vars_)))
+        polys.append(terms)
+    polys.append([Monomial(one, tuple((v, 1) for v in range(n))), Monomial(-one, ())])
+    return PolySystem(n, polys)
+
+
+def chandrasekhar_system(n: int, level: PrecisionLevel, c: Fraction = Fraction(33, 64)) -> PolySystem:
+    """Discretized H-equation (bench.py:19-43); the weights i/(i+j) and
+    -(c*w) are formed in working precision on the GPU."""
+    from .varith import VecContext
+    if n < 1:
+        raise ValueError("need n >= 1")
+    ctx = VecContext(level)
+    c_val = level.from_fraction(c)
+    two_n = level.from_int(2 * n)
+    num = level.to_planes([level.from_int(i) for i in range(1, n + 1) for _ in range(n)])
+    den = level.to_planes([level.from_int(i + j) for i in range(1, n + 1) for j in range(n)])
+    w = ctx.div(num, den)
+    cw = ctx.mul(np.repeat(level.to_planes([c_val]), n * n, axis=-1), w)
+    coeffs = level.from_planes(-cw)
+    polys = []
+    for i in range(1, n + 1):
+        terms = [Monomial(two_n, ((i - 1, 1),)), Monomial(-two_n, ())]
+        for j in range(n):
+            coeff = coeffs[(i - 1) * n + j]
+            exps = ((i - 1, 2),) if j == i - 1 else tuple(sorted(((i - 1, 1), (j, 1))))
+            terms.append(Monomial(coeff, exps))
+        polys.append(terms)
+    return PolySystem(n, polys)
+
+
+def chandrasekhar_start(n: int, level: PrecisionLevel) -> list:
+    return [level.one() for _ in range(n)]
+
+
+def random_stress_products(m: int, n: int, seed: int, level: PrecisionLevel) -> list:
+    """m random coefficients on the full degree-n product (bench.py:98-110)."""
+    rng = random.Random(seed)
+    exps = tuple((v, 1) for v in range(n))
+    out = []
+    for _ in range(m):
+        if level.cplx:
+            coeff = level.from_float(rng.uniform(0.5, 2.0), rng.uniform(0.5, 2.0))
+        else:
+            coeff = level.from_float(rng.uniform(0.5, 2.0))
+        out.append(Monomial(coeff, exps))
+    return out
