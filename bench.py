@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Newton steps/s at dimension 1024 (eval + diff + MGS least squares + update)
+on B200, per BASELINE.json: F(1024, 1024, 32) random sparse system (SURVEY
+8(d)), complex quad double by default (--base d/dd/qd).
+
+One JSON line on rank 0.  `value` is device-resident throughput (inputs in
+HBM, CUDA events on the launching stream, max over ranks); `e2e` is the same
+step through the C ABI with host buffers (h2d of x, d2h of x_next, f, dx and
+the norms inside the timed region).  Multi-GPU runs are independent replicas
+(a single system does not shard); `value` sums them.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Newton steps/sec (eval+diff+MGS) at dim 1024 in complex d/dd/qd; quality-up ratio"
+R_ADD = {1: 1, 2: 20, 4: 87}   # FP64 instructions of a real add
+R_MUL = {1: 1, 2: 9, 4: 185}   # ... of a real multiply with FMA two_prod
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--base", default="qd", choices=["d", "dd", "qd"])
+    ap.add_argument("--dim", type=int, default=1024)
+    ap.add_argument("--terms", type=int, default=1024)
+    ap.add_argument("--k", type=int, default=32)
+    ap.add_argument("--rows", type=int, default=None, help="equations m (default = dim)")
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def level_costs(nc: int, cplx: bool):
+    radd, rmul = R_ADD[nc], R_MUL[nc]
+    if cplx:
+        return {"add": 2 * radd, "mul": 4 * rmul + 2 * radd, "int": 2 * rmul, "radd": radd, "rmul": rmul}
+    return {"add": radd, "mul": rmul, "int": rmul, "radd": radd, "rmul": rmul}
+
+
+def work_counts(stats, nc: int, cplx: bool, m: int, n: int):
+    """Algorithmic FP64 instruction counts and bytes of one step."""
+    c = level_costs(nc, cplx)
+    w_eval = (stats.mul_ops * c["mul"] + stats.int_mul_ops * c["int"] + stats.add_ops * c["add"]
+              + stats.table_mul_ops * c["mul"])
+    U = m * n * (n + 1) // 2                      # MGS update elements
+    w_mgs = (U * (2 * c["mul"] + 2 * c["add"])    # r_kj dot + a -= q r
+             + (2 * n + 1) * m * (2 * c["rmul"] + 2 * c["radd"]) // (1 if cplx else 2)  # norms
+             + n * m * (2 if cplx else 1) * c["rmul"]                                    # q = a / r
+             + n * (n - 1) // 2 * (c["mul"] + c["add"]))                                 # back-sub
+    es = nc * (2 if cplx else 1)
+    b_eval = (stats.support * 8 + (stats.monomials + 1) * 4 + stats.monomials * es * 8
+              + (n + m) * es * 8 + m * n * es * 8)
+    return w_eval, w_mgs, b_eval
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port (oracle/pn_oracle.c) on a bounded sample
+
+def cpu_step_estimate(args, packed, x_planes, budget: float):
+    """Seconds of one full Newton step of the oracle, from a timed row sample
+    of the evaluation and a smaller MGS (cubic extrapolation)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    threads = os.cpu_count() or 1
+    L = oracle.Level(packed.level.base, packed.level.cplx)
+    csr = oracle.CSR.from_packed(packed)
+    m, n = packed.n_eqs, packed.n_vars
+    # evaluation: rows are independent (evaldiff.py:252-265)
+    rows = max(1, threads)
+    sub = csr.rows(range(rows)).canonical()
+    t0 = time.perf_counter()
+    oracle.evaluate(L, sub, x_planes, nthreads=threads, canonical=True)
+    t_rows = time.perf_counter() - t0
+    reps = 1
+    if t_rows < budget * 0.3:
+        more = int(min(m, rows * max(1, (budget * 0.4) / max(t_rows, 1e-3))))
+        if more > rows:
+            sub = csr.rows(range(more)).canonical()
+            t0 = time.perf_counter()
+            oracle.evaluate(L, sub, x_planes, nthreads=threads, canonical=True)
+            t_rows = time.perf_counter() - t0
+            rows = more
+    del reps
+    t_eval = t_rows * m / rows
+    # MGS: s x s sample, scaled by m n^2
+    s = 64
+    rng = np.random.default_rng(1)
+    while True:
+        aug = np.ascontiguousarray(rng.uniform(-1, 1, L.cshape + (s, s + 1)))
+        t0 = time.perf_counter()
+        oracle.least_squares(L, aug, nthreads=threads)
+        t_s = time.perf_counter() - t0
+        if t_s > budget * 0.15 or s >= min(m, n):
+            break
+        s = min(min(m, n), s * 2)
+    t_mgs = t_s * (m * n * (n + 1)) / (s * s * (s + 1))
+    sample = (f"oracle/pn_oracle.c (-O2, OpenMP {threads} threads): evaluation of {rows} of {m} rows "
+              f"({t_rows:.2f} s, scaled x{m / rows:.1f}) + MGS least squares {s}x{s} ({t_s:.2f} s, scaled by "
+              f"m*n^2 x{(m * n * (n + 1)) / (s * s * (s + 1)):.0f}); extrapolated")
+    return t_eval + t_mgs, threads, sample, {"eval_s": t_eval, "mgs_s": t_mgs}
+
+
+# ---------------------------------------------------------------------------
+
+def build_inputs(args, rank=0):
+    from paper_1402_2626_b200.generators import random_sparse_system
+    from paper_1402_2626_b200.xprec import precision_level
+    level = precision_level(args.base, True)
+    m = args.rows or args.dim
+    packed = random_sparse_system(args.dim, args.terms, args.k, level, seed=args.seed, m=m)
+    rng = np.random.default_rng(args.seed + 1)
+    x = rng.uniform(0.5, 2.0, level.cshape + (args.dim,)) * rng.choice([-1.0, 1.0], level.cshape + (args.dim,))
+    x[:, 1:] = 0.0  # level.from_float values (SURVEY 8(d) random_point)
+    return level, packed, np.ascontiguousarray(x)
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    level, packed, x = build_inputs(args)
+    cfg = {"workload": f"F({args.dim},{args.terms},{args.k}) complex {args.base} Newton step "
+                       f"{args.rows or args.dim}x{args.dim}", "m": args.rows or args.dim, "n": args.dim,
+           "terms_per_poly": args.terms, "k": args.k, "precision": f"complex {args.base}"}
+    per_step_budget = max(3.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, cores, sample, parts = cpu_step_estimate(args, packed, x, per_step_budget)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    v = 1.0 / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_s": parts}))
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1402_2626_b200 import _lib
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+
+    lib = _lib.load()
+    _lib.require_gpu()
+    level, packed, x_host = build_inputs(args, rank)
+    m, n = packed.n_eqs, packed.n_vars
+    es, nc = level.es, level.ncomp
+    t_prep = time.perf_counter()
+    prep = PreparedSystem(packed)
+    t_prep = time.perf_counter() - t_prep
+    stats = prep.stats()
+    w_eval, w_mgs, b_eval = work_counts(stats, nc, level.cplx, m, n)
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x_d = torch.from_numpy(x_host).to(dev)
+    outs = {k: torch.empty(s, dtype=torch.float64, device=dev) for k, s in
+            [("xn", (es, n)), ("f", (es, m)), ("dx", (es, n)), ("fm", (nc, m)), ("dm", (nc, n)), ("xm", (nc, n))]}
+    info = _lib.NumInfo()
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step():
+        rc = lib.pn_newton_step(prep.handle, _lib.ptr(x_d), _lib.ptr(outs["xn"]), _lib.ptr(outs["f"]),
+                                _lib.ptr(outs["dx"]), _lib.ptr(outs["fm"]), _lib.ptr(outs["dm"]),
+                                _lib.ptr(outs["xm"]), ctypes.byref(info), ctypes.c_void_p(stream))
+        _lib.check(rc, info)
+        return info.t_evaluate, info.t_solve, info.t_update
+
+    peak = ctypes.c_double(0)
+    _lib.check(lib.pn_fp64_peak(ctypes.byref(peak), ctypes.c_void_p(stream)))
+    fp64_peak = peak.value
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = []
+    e0.record()
+    for _ in range(args.steps):
+        phases.append(step())
+    e1.record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+        torch.distributed.barrier()
+    sec_step = elapsed / args.steps
+    value = world * args.steps / elapsed
+
+    # end to end through the C ABI with host buffers (pinned)
+    ke = args.e2e_steps or max(2, min(args.steps, 5))
+    pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    xh = pin((es, n))
+    xh[...] = x_host.reshape(es, n)
+    ho = {k: pin(tuple(v.shape)) for k, v in outs.items()}
+
+    def step_host():
+        rc = lib.pn_newton_step(prep.handle, _lib.ptr(xh), _lib.ptr(ho["xn"]), _lib.ptr(ho["f"]),
+                                _lib.ptr(ho["dx"]), _lib.ptr(ho["fm"]), _lib.ptr(ho["dm"]), _lib.ptr(ho["xm"]),
+                                ctypes.byref(info), ctypes.c_void_p(stream))
+        _lib.check(rc, info)
+
+    step_host()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(ke):
+        step_host()
+    e3.record()
+    torch.cuda.synchronize()
+    e2e_elapsed = e2.elapsed_time(e3) / 1e3
+    if world > 1:
+        t = torch.tensor([e2e_elapsed], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_elapsed = float(t.item())
+    h2d = xh.nbytes
+    d2h = sum(v.nbytes for v in ho.values())
+
+    t_eval = statistics.median(p[0] for p in phases)
+    t_solve = statistics.median(p[1] for p in phases)
+    t_upd = statistics.median(p[2] for p in phases)
+    mgs_rate = w_mgs / t_solve
+    roofline = {"bound": "fp64", "kernel": "k_mgs_sweep (MGS least squares phase)",
+                "achieved": mgs_rate / 1e12, "peak": fp64_peak / 1e12, "unit": "T FP64-instr/s",
+                "frac": mgs_rate / fp64_peak, "traffic": None,
+                "peak_source": "measured in-run DFMA probe (pn_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
+                "work_fp64_instr": w_mgs}
+    evalr = {"kernel": "k_mono_tree + k_segments (eval+diff phase)", "seconds": t_eval,
+             "achieved_fp64": w_eval / t_eval / 1e12, "frac_fp64": w_eval / t_eval / fp64_peak,
+             "achieved_gbs": b_eval / t_eval / 1e9, "work_fp64_instr": w_eval, "bytes": b_eval}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_cpu, cores, sample, parts = cpu_step_estimate(args, packed, x_host, args.cpu_budget)
+        cpu = {"value": 1.0 / t_cpu, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample,
+               "phases_s": parts}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"F({args.dim},{args.terms},{args.k}) complex {args.base} Newton step "
+                                   f"{m}x{n} (eval+diff+MGS+update), x fixed per step",
+                       "m": m, "n": n, "terms_per_poly": args.terms, "k": args.k,
+                       "precision": f"complex {args.base}", "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (supports + contributions > 126 MB per step)"},
+            "e2e": {"value": world * ke / e2e_elapsed, "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "eval_roofline": evalr,
+            "phases_ms": {"evaluate": t_eval * 1e3, "solve": t_solve * 1e3, "update": t_upd * 1e3},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "prepare_s": t_prep,
+        }
+        if cpu:
+            out["quality_up_same_precision"] = value / cpu["value"]
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

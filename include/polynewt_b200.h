@@ -101,6 +101,9 @@ const char *pn_last_error(void);
 int pn_device_count(int *count);
 /* number of kernels this library launched since load (bench evidence) */
 int64_t pn_launch_count(void);
+/* measured FP64 pipe throughput of the current device (DFMA instructions/s),
+ * the roofline denominator for the FP64-bound kernels */
+int pn_fp64_peak(double *instr_per_s, void *stream);
 
 /* ---- element-wise arithmetic on component planes ---------------------- */
 /* a, b, out: planes of n elements.  b may be NULL for unary ops.  For

@@ -55,6 +55,7 @@ SIGNATURES = {
     "pn_last_error": ([], ctypes.c_char_p),
     "pn_device_count": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "pn_launch_count": ([], ctypes.c_int64),
+    "pn_fp64_peak": ([ctypes.POINTER(ctypes.c_double), ctypes.c_void_p], ctypes.c_int),
     "pn_vec_op": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                    ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "pn_tree_sum": ([ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],

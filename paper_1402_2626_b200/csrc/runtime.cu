@@ -287,9 +287,51 @@ __global__ void k_tree_sum(long long n, const double *__restrict__ a, double *__
   }
 }
 
+// FP64 pipe throughput probe: every thread runs 8 independent DFMA chains;
+// one DFMA is counted as one FP64 instruction (the unit of the roofline's
+// work counts).  The result is written so the chains cannot be elided.
+__global__ void __launch_bounds__(256) k_fp64_probe(int iters, double seed, double *out) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+  const double b = 0.999999, c = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace pn
 
 using namespace pn;
+
+extern "C" int pn_fp64_peak(double *instr_per_s, void *stream) {
+  PN_API_BEGIN
+  PN_REQUIRE(instr_per_s, PN_E_ARG, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf sink(64, st);
+  const int iters = 1 << 14, threads = 256, blocks = num_sms() * 8;
+  cudaEvent_t e0, e1;
+  PN_CHECK_CUDA(cudaEventCreate(&e0));
+  PN_CHECK_CUDA(cudaEventCreate(&e1));
+  k_fp64_probe<<<blocks, threads, 0, st>>>(iters / 8, 1.0, sink.d());  // warm-up
+  PN_CHECK_CUDA(cudaEventRecord(e0, st));
+  k_fp64_probe<<<blocks, threads, 0, st>>>(iters, 1.0, sink.d());
+  PN_CHECK_CUDA(cudaEventRecord(e1, st));
+  PN_CHECK_LAUNCH();
+  count_launch(2);
+  PN_CHECK_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  PN_CHECK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *instr_per_s = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+  PN_API_END
+}
 
 extern "C" {
 

@@ -1,0 +1,166 @@
+"""Host-side logic and the C ABI surface (CPU only: no kernel launches)."""
+
+import ctypes
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+HEADER = os.path.join(ROOT, "include", "polynewt_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(pn_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1402_2626_b200 import _lib
+    lib = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert lib.pn_version() >= 100
+
+
+def test_no_device_is_reported_not_faked():
+    from paper_1402_2626_b200 import _lib
+    n = _lib.device_count()
+    assert n >= 0
+    if n == 0:
+        with pytest.raises(RuntimeError):
+            _lib.require_gpu()
+
+
+def test_error_codes_map_to_reference_exceptions():
+    from paper_1402_2626_b200 import _lib
+    from paper_1402_2626_b200.mgs import MgsBreakdownError, SingularMatrixError
+    info = _lib.NumInfo(k=3, index=5, rkk=1e-40, threshold=1e-30)
+    with pytest.raises(MgsBreakdownError) as e:
+        _lib.check(_lib.PN_E_BREAKDOWN, info)
+    assert e.value.k == 3
+    with pytest.raises(SingularMatrixError) as e:
+        _lib.check(_lib.PN_E_SINGULAR, info)
+    assert e.value.index == 5
+    with pytest.raises(ValueError):
+        _lib.check(_lib.PN_E_ARG)
+
+
+def test_argument_validation_without_gpu():
+    """pn_system_create validates supports like Monomial/PolySystem before
+    touching the device."""
+    from paper_1402_2626_b200 import _lib
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    pp = np.array([0, 1], np.int32)
+    mp = np.array([0, 2], np.int32)
+    vi = np.array([3, 1], np.int32)  # not increasing
+    ex = np.array([1, 1], np.int32)
+    co = np.ones((2, 1, 1))
+    rc = lib.pn_system_create(1, 1, 1, 4, 1, 2, _lib.ptr(pp), _lib.ptr(mp), _lib.ptr(vi), _lib.ptr(ex),
+                              _lib.ptr(co), 0, ctypes.byref(h))
+    assert rc == _lib.PN_E_ARG
+    assert "strictly increasing" in _lib.last_error()
+    vi = np.array([1, 9], np.int32)  # out of range
+    rc = lib.pn_system_create(1, 1, 1, 4, 1, 2, _lib.ptr(pp), _lib.ptr(mp), _lib.ptr(vi), _lib.ptr(ex),
+                              _lib.ptr(co), 0, ctypes.byref(h))
+    assert rc == _lib.PN_E_ARG and "out of range" in _lib.last_error()
+
+
+def test_generator_is_deterministic_and_valid():
+    from paper_1402_2626_b200.generators import random_sparse_system
+    from paper_1402_2626_b200.xprec import precision_level
+    level = precision_level("dd", True)
+    a = random_sparse_system(64, 16, 8, level, seed=3, maxexp=3)
+    b = random_sparse_system(64, 16, 8, level, seed=3, maxexp=3)
+    assert np.array_equal(a.var_idx, b.var_idx) and np.array_equal(a.coeffs, b.coeffs)
+    assert a.monomials == 64 * 16 and a.support == 64 * 16 * 8
+    k = np.diff(a.mon_ptr)
+    assert np.all(k == 8)
+    for c in range(0, a.monomials, 37):
+        v = a.var_idx[a.mon_ptr[c]:a.mon_ptr[c + 1]]
+        assert np.all(np.diff(v) > 0) and v.min() >= 0 and v.max() < 64
+    assert a.exps.min() >= 1 and a.exps.max() <= 3
+    mag = np.abs(a.coeffs[:, 0])
+    assert mag.min() >= 0.5 and mag.max() < 2.0
+    assert np.all(a.coeffs[:, 1] == 0.0)
+
+
+def test_canonical_sparse_key_equals_dense_key():
+    # the sparse key orders like the dense exponent vector
+    from paper_1402_2626_b200.polyrep import Monomial
+    rng = np.random.default_rng(0)
+    mons = []
+    for _ in range(300):
+        k = int(rng.integers(0, 5))
+        vs = sorted(rng.choice(12, size=k, replace=False).tolist())
+        mons.append(Monomial(1.0, tuple((v, int(rng.integers(1, 3))) for v in vs)))
+    dense = sorted(range(300), key=lambda i: mons[i].exponent_key(12))
+    sparse = sorted(range(300), key=lambda i: mons[i].sparse_key())
+    assert dense == sparse
+
+
+def test_monomial_validation():
+    from paper_1402_2626_b200.polyrep import Monomial, PolySystem
+    from paper_1402_2626_b200.xprec import precision_level
+    dd = precision_level("dd", False)
+    with pytest.raises(ValueError):
+        Monomial(dd.zero(), ((0, 1),))
+    with pytest.raises(ValueError):
+        Monomial(dd.one(), ((1, 1), (0, 1)))
+    with pytest.raises(ValueError):
+        Monomial(dd.one(), ((0, 0),))
+    with pytest.raises(ValueError):
+        PolySystem(2, [[Monomial(dd.one(), ((2, 1),))]])
+
+
+def test_precision_level_and_scalars():
+    from paper_1402_2626_b200.xprec import (DoubleDouble, QuadDouble, precision_level, render_decimal)
+    cqd = precision_level("qd", True)
+    assert cqd.cshape == (2, 4) and cqd.es == 8 and cqd.eps == 2.0 ** -209
+    x = cqd.from_float(1.5, -2.0)
+    assert cqd.to_components(x) == [1.5, 0, 0, 0, -2.0, 0, 0, 0]
+    assert cqd.from_components(cqd.to_components(x)) == x
+    third = precision_level("dd", False).from_fraction(Fraction(1, 3))
+    assert third.comps[0] == 1 / 3 and third.comps[1] != 0.0
+    assert render_decimal(third).startswith("3.333333333333333333333333333333")
+    assert float(QuadDouble(1.0, 2.0 ** -60)) == 1.0
+    assert DoubleDouble(-0.0).comps == (0.0, 0.0)
+    planes = cqd.to_planes([x, -x])
+    assert planes.shape == (2, 4, 2)
+    assert cqd.from_planes(planes) == [x, -x]
+
+
+def test_reference_scalars_are_accepted_by_packing():
+    """Coefficients may be the reference's own objects (duck typing)."""
+    from paper_1402_2626_b200.polyrep import Monomial, PackedSystem, PolySystem
+    from paper_1402_2626_b200.xprec import precision_level
+
+    class RefDD:  # stand-in with the reference's attribute layout
+        def __init__(self, hi, lo=0.0):
+            self.comps = (hi, lo)
+
+    class RefComplex:
+        def __init__(self, re, im):
+            self.re, self.im = re, im
+
+    cdd = precision_level("dd", True)
+    sys_ = PolySystem(3, [[Monomial(RefComplex(RefDD(1.0), RefDD(2.0)), ((0, 1), (2, 2)))]])
+    p = PackedSystem.from_system(sys_, cdd)
+    assert p.coeffs.shape == (2, 2, 1)
+    assert p.coeffs[0, 0, 0] == 1.0 and p.coeffs[1, 0, 0] == 2.0
+    assert p.var_idx.tolist() == [0, 2] and p.exps.tolist() == [1, 2]
+
+
+def test_golden_fixture_manifest():
+    import json
+    names = json.load(open(os.path.join(ROOT, "tests", "golden", "MANIFEST.json")))
+    assert len(names) >= 40
+    g = golden("newton_c1")
+    assert int(g["n_vars"]) == 32 and g["poly_ptr"][-1] == 32 * 32
