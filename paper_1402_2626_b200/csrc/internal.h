@@ -111,7 +111,8 @@ struct MgsStatus {
 struct MgsWork {
   DevArena qbuf;    // normalized pivot columns when Q is not requested
   DevArena orig;    // orig column norms (hi)
-  DevArena status;  // int32[4] + double[4]
+  DevArena status;  // MgsStatus
+  DevArena ready;   // dataflow schedule: pivot-published flags (n+1 ints)
 };
 void mgs_factor_device(int nc, int cplx, int m, int n, double *A, double *Q, double *R, MgsWork &w,
                        cudaStream_t st);

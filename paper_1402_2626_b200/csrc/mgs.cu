@@ -18,6 +18,9 @@
 // Each CTA handles one column at a time; thread t owns the aligned row block
 // [t*B, t*B+B), so dot products and norms reduce in the reference's
 // canonical pairwise order (block_tree_reduce) and are bit-identical.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -158,6 +161,419 @@ __global__ void __launch_bounds__(kMgsThreads) k_mgs_sweep(double *__restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent dataflow form of the same sweeps: one launch for the whole
+// factorisation.  Column j is owned by CTA j mod G; a CTA applies sweep k to
+// its columns as soon as pivot q_k is published (ready[k]), and the owner of
+// column k+1 updates that column first, normalises it and publishes q_{k+1}.
+// Every column still receives its updates in sweep order with the same
+// reductions, so the result is bit-identical to the launch-per-sweep path;
+// only the idle gaps between sweeps disappear.  All CTAs are co-resident
+// (cooperative launch), so the waits cannot deadlock; a clock64 watchdog
+// turns a stuck wait into an error instead of a hang.
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class E, int B>
+__device__ __forceinline__ void load_rows_cg(E (&v)[B], const double *__restrict__ col, int row0, int m) {
+  constexpr int es = Traits<E>::es;
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    E x = ezero<E>();
+    if (row0 + q < m) {
+      double *d = reinterpret_cast<double *>(&x);
+      const double2 *s = reinterpret_cast<const double2 *>(col + (long long)(row0 + q) * es);
+      if constexpr (es % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < es / 2; ++i) {
+          double2 t = __ldcg(s + i);
+          d[2 * i] = t.x;
+          d[2 * i + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < es; ++i) d[i] = __ldcg(col + (long long)(row0 + q) * es + i);
+      }
+    }
+    v[q] = x;
+  }
+}
+
+// publish pivot k: make this CTA's Q/R writes visible, then raise the flag
+__device__ __forceinline__ void publish(int *ready, int k) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(ready + k, 1);
+}
+
+// wait for pivot k; false on failure (breakdown elsewhere or watchdog)
+__device__ __forceinline__ bool wait_pivot(const int *ready, int k, MgsStatus *status) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    long long t0 = clock64();
+    int ok = 1;
+    while (ld_acquire(ready + k) == 0) {
+      __nanosleep(64);
+      if (ld_acquire(&status->code) != 0) {  // a breakdown ended the factorisation
+        ok = 0;
+        break;
+      }
+      if (clock64() - t0 > (1ll << 36)) {  // ~30 s at 2 GHz: never on a healthy run
+        status->k = k;
+        atomicExch(&status->code, PN_E_CUDA);
+        ok = 0;
+        break;
+      }
+    }
+    if (ok && ld_acquire(&status->code) != 0) ok = 0;
+    s_ok = ok;
+  }
+  __syncthreads();
+  const bool ok = s_ok;
+  __syncthreads();
+  return ok;
+}
+
+template <class E, int B>
+__global__ void __launch_bounds__(kMgsThreads) k_mgs_dataflow(double *__restrict__ A, int m, int n,
+                                                              double *__restrict__ orig, double eps,
+                                                              double *__restrict__ Q, double *__restrict__ R,
+                                                              MgsStatus *status, int *ready) {
+  using Rl = typename Traits<E>::R;
+  constexpr int es = Traits<E>::es;
+  __shared__ E sme[kMgsThreads / 32];
+  __shared__ Rl smr[kMgsThreads / 32];
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int row0 = threadIdx.x * B;
+  const int valid = m - row0 < 0 ? 0 : (m - row0 > B ? B : m - row0);
+  const int nparts = (m + B - 1) / B;
+  // initial column norms of the owned columns (mgs.py:171-172)
+  for (int j = cta; j < n; j += G) {
+    E v[B];
+    load_rows<E, B>(v, A + (long long)j * m * es, row0, m);
+    Rl nrm = column_norm<E, B>(v, row0, m, smr);
+    if (threadIdx.x == 0) orig[j] = nrm.c[0];
+  }
+  __syncthreads();
+  if (cta == 0) {  // pivot 0
+    E v[B];
+    load_rows<E, B>(v, A, row0, m);
+    Rl rkk = column_norm<E, B>(v, row0, m, smr);
+    finish_pivot<E, B>(v, row0, m, n, 0, rkk, orig, eps, Q, R, status);
+    publish(ready, 0);
+  }
+  for (int k = 0; k < n; ++k) {
+    // first owned column after k
+    int j0 = k + 1 + (((cta - (k + 1)) % G) + G) % G;
+    if (j0 > n) break;
+    if (!wait_pivot(ready, k, status)) return;
+    E qv[B];
+    load_rows_cg<E, B>(qv, Q + (long long)k * m * es, row0, m);
+    for (int j = j0; j <= n; j += G) {
+      double *col = A + (long long)j * m * es;
+      E a[B], pr[B];
+      load_rows<E, B>(a, col, row0, m);
+#pragma unroll
+      for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), a[q]);
+      E part = local_tree<E, B>(pr, valid);
+      const E r = block_tree_reduce<E, kMgsThreads>(part, nparts, sme);
+#pragma unroll
+      for (int q = 0; q < B; ++q) a[q] = esub(a[q], emul(qv[q], r));
+      store_rows<E, B>(col, a, row0, m);
+      if (threadIdx.x == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
+      if (j == k + 1) {
+        Rl rkk = column_norm<E, B>(a, row0, m, smr);
+        const bool ok = finish_pivot<E, B>(a, row0, m, n, k + 1, rkk, orig, eps, Q, R, status);
+        publish(ready, k + 1);  // also on breakdown, so that waiters wake up
+        if (!ok) return;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_mgs_flow: the production schedule.  Same dataflow as k_mgs_dataflow, plus
+//  * priority: each CTA always serves its lowest unfinished column first (the
+//    next pivot on the critical path); while that column waits for a pivot,
+//    the CTA catches its other columns up on every published sweep, checking
+//    between sweeps whether the critical column can move again;
+//  * the working column lives in shared memory (component planes, XOR
+//    swizzled so thread t's aligned row block is bank-conflict free) and
+//    stays there across consecutive sweeps; q_k rows stream from L2.  Few
+//    live registers -> two CTAs per SM even in complex quad double.
+// Per column the operation sequence is exactly the reference's, so results
+// are bit-identical to both other schedules.
+
+// element load through L2 only (pivots written by other CTAs in this launch)
+template <class E>
+__device__ __forceinline__ E eload_cg(const double *p) {
+  E r;
+  double *d = reinterpret_cast<double *>(&r);
+  constexpr int es = Traits<E>::es;
+  if constexpr (es % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < es / 2; ++i) {
+      const double2 t = __ldcg(reinterpret_cast<const double2 *>(p) + i);
+      d[2 * i] = t.x;
+      d[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < es; ++i) d[i] = __ldcg(p + i);
+  }
+  return r;
+}
+
+template <class E, int B>
+struct SmemCol {
+  double *base;  // es planes of NT*B doubles
+  int plane;
+  __device__ __forceinline__ int pos(int r) const {
+    constexpr int W = (32 / B) > 0 ? 32 / B : 1;
+    const int t = r / B, i = r % B;
+    return t * B + (i ^ ((t / W) % B));
+  }
+  __device__ __forceinline__ E get(int r) const {
+    E v;
+    double *d = reinterpret_cast<double *>(&v);
+    const int p = pos(r);
+#pragma unroll
+    for (int c = 0; c < Traits<E>::es; ++c) d[c] = base[c * plane + p];
+    return v;
+  }
+  __device__ __forceinline__ void put(int r, const E &v) const {
+    const double *d = reinterpret_cast<const double *>(&v);
+    const int p = pos(r);
+#pragma unroll
+    for (int c = 0; c < Traits<E>::es; ++c) base[c * plane + p] = d[c];
+  }
+};
+
+// streaming pairwise tree (binary counter) over a thread's aligned row block
+template <class E, int D>
+struct Pairwise {
+  E st[D];
+  int cnt = 0;
+  __device__ __forceinline__ void push(E v) {
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      if (!((cnt >> l) & 1)) {
+        st[l] = v;
+        break;
+      }
+      v = eadd(st[l], v);
+    }
+    ++cnt;
+  }
+  __device__ __forceinline__ E fold() const {
+    E acc = ezero<E>();
+    bool have = false;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      if ((cnt >> l) & 1) {
+        acc = have ? eadd(st[l], acc) : st[l];
+        have = true;
+      }
+    }
+    return acc;
+  }
+};
+
+template <int B> struct Depth { static constexpr int value = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 3 : B <= 8 ? 4 : 5; };
+
+template <class E, int B, int NT>
+__global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
+                                                    double eps, double *__restrict__ Q, double *__restrict__ R,
+                                                    MgsStatus *status, int *ready) {
+  using Rl = typename Traits<E>::R;
+  constexpr int es = Traits<E>::es;
+  constexpr int D = Depth<B>::value;
+  extern __shared__ __align__(16) double smem_col[];
+  __shared__ E sme[NT / 32];
+  __shared__ Rl smr[NT / 32];
+  __shared__ int s_done[64];
+  __shared__ int s_known, s_fail, s_res;
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int row0 = tid * B;
+  const int nparts = (m + B - 1) / B;
+  const int nown = cta <= n ? (n - cta) / G + 1 : 0;
+  const SmemCol<E, B> col{smem_col, NT * B};
+  if (nown == 0) return;
+  if (tid == 0) {
+    s_known = 0;
+    s_fail = 0;
+    s_res = -1;
+  }
+  for (int i = tid; i < nown && i < 64; i += NT) s_done[i] = 0;
+  __syncthreads();
+
+  // load / store the resident column (coalesced over elements)
+  auto load_col = [&](int j) {
+    const double *g = A + (long long)j * m * es;
+    for (int r = tid; r < m; r += NT) col.put(r, eload<E>(g + (long long)r * es));
+  };
+  auto store_col = [&](int j) {
+    double *g = A + (long long)j * m * es;
+    for (int r = tid; r < m; r += NT) estore(g + (long long)r * es, col.get(r));
+  };
+  auto make_resident = [&](int idx) {
+    if (s_res != idx) {
+      __syncthreads();
+      if (s_res >= 0) store_col(cta + s_res * G);
+      __syncthreads();
+      load_col(cta + idx * G);
+      __syncthreads();
+      if (tid == 0) s_res = idx;
+      __syncthreads();
+    }
+  };
+  // advance the CTA-wide count of published pivots (non-blocking)
+  auto poll = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      int kn = s_known;
+      while (kn < n && ld_acquire(ready + kn)) ++kn;
+      s_known = kn;
+      if (ld_acquire(&status->code)) s_fail = 1;
+    }
+    __syncthreads();
+  };
+  auto block_wait = [&](int k) {
+    __syncthreads();
+    if (tid == 0) {
+      long long t0 = clock64();
+      while (!ld_acquire(ready + k)) {
+        if (ld_acquire(&status->code)) break;
+        __nanosleep(100);
+        if (clock64() - t0 > (1ll << 36)) {
+          status->k = k;
+          atomicExch(&status->code, PN_E_CUDA);
+          break;
+        }
+      }
+    }
+    poll();
+  };
+  // one sweep k applied to the resident column j (mgs.py:201-215)
+  auto apply = [&](int k, int j) {
+    const double *qk = Q + (long long)k * m * es;
+    Pairwise<E, D> pw;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int r = row0 + q;
+      if (r < m) pw.push(emul(econj(eload_cg<E>(qk + (long long)r * es)), col.get(r)));
+    }
+    const E rk = block_tree_reduce<E, NT>(pw.fold(), nparts, sme);
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int r = row0 + q;
+      if (r < m) col.put(r, esub(col.get(r), emul(eload_cg<E>(qk + (long long)r * es), rk)));
+    }
+    if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, rk);
+  };
+  // norm of the resident column (mgs.py:128-137)
+  auto norm = [&]() -> Rl {
+    Pairwise<Rl, D> pw;
+#pragma unroll
+    for (int q = 0; q < B; ++q)
+      if (row0 + q < m) pw.push(eabs2(col.get(row0 + q)));
+    return fsqrt(block_tree_reduce<Rl, NT>(pw.fold(), nparts, smr));
+  };
+
+  // phase 0: initial norms of the owned columns (mgs.py:171-172)
+  for (int i = 0; i < nown; ++i) {
+    const int j = cta + i * G;
+    if (j >= n) break;
+    make_resident(i);
+    const Rl nrm = norm();
+    if (tid == 0) orig[j] = nrm.c[0];
+  }
+
+  int lo = 0;
+  while (lo < nown) {
+    const int c = cta + lo * G;
+    poll();
+    if (s_fail) return;
+    int dlo = s_done[lo];
+    if (dlo < c && dlo >= s_known) {
+      // critical column blocked on pivot dlo: catch a lagging column up
+      int pick = -1;
+      for (int i = lo + 1; i < nown; ++i)
+        if (s_done[i] < s_known) {
+          pick = i;
+          break;
+        }
+      if (pick < 0) {
+        block_wait(dlo);
+        continue;
+      }
+      make_resident(pick);
+      const int cj = cta + pick * G;
+      int d = s_done[pick];
+      while (d < s_known && d < cj) {
+        apply(d, cj);
+        ++d;
+        poll();
+        if (s_fail) return;
+        if (s_known > s_done[lo]) break;  // the critical column can move again
+      }
+      __syncthreads();
+      if (tid == 0) s_done[pick] = d;
+      __syncthreads();
+      continue;
+    }
+    // serve the critical column with every published sweep
+    make_resident(lo);
+    int d = dlo;
+    while (d < c) {
+      if (d >= s_known) {
+        poll();
+        if (s_fail) return;
+        if (d >= s_known) break;  // next pivot not out yet: reconsider the work list
+      }
+      apply(d, c);
+      ++d;
+    }
+    __syncthreads();
+    if (tid == 0) s_done[lo] = d;
+    __syncthreads();
+    if (d < c) continue;
+    // pivot c (mgs.py:176-193); c == n is the residual norm z
+    const Rl rkk = norm();
+    if (c < n) {
+      const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), orig[c]);
+      if (rkk.c[0] <= thr) {
+        if (tid == 0) {
+          status->k = c;
+          status->rkk = rkk.c[0];
+          status->thr = thr;
+          __threadfence();
+          atomicExch(&status->code, PN_E_BREAKDOWN);
+        }
+        publish(ready, c);
+        return;
+      }
+    }
+    if (tid == 0) estore(R + ((long long)c * (n + 1) + c) * es, eembed(rkk, (E *)nullptr));
+    if (c < n) {
+      const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+      double *qc = Q + (long long)c * m * es;
+      for (int r = tid; r < m; r += NT) estore(qc + (long long)r * es, ediv_prepared(col.get(r), p));
+      publish(ready, c);
+    }
+    __syncthreads();
+    if (tid == 0) s_res = -1;  // column c is final; nothing to write back
+    ++lo;
+  }
+}
+
 // back substitution R x = y, y = R[:n, n] (mgs.py:229-247): descending j,
 // x_j = y_j / r_jj (full complex division), y[:j] -= R[:j, j] x_j.  The
 // division's reciprocal depends on r_jj only, so it is prepared for all j
@@ -222,13 +638,58 @@ __global__ void __launch_bounds__(NT) k_backsub(const double *__restrict__ R, in
 
 static double level_eps(int nc) { return nc == 1 ? 0x1p-53 : nc == 2 ? 0x1p-104 : 0x1p-209; }
 
+// PN_MGS_MODE=sweeps selects the launch-per-sweep schedule (kept as the
+// reference schedule for tests); the default is the persistent dataflow kernel.
+// 0 flow, 1 dataflow, 2 sweeps.  Default by measurement (profiles/r01): the
+// priority/smem schedule wins when sweeps are compute-heavy (quad double);
+// the plain dataflow kernel has the shorter per-sweep latency for d/dd.
+static int mgs_mode(int nc) {
+  const char *v = getenv("PN_MGS_MODE");
+  if (v && strcmp(v, "sweeps") == 0) return 2;
+  if (v && strcmp(v, "dataflow") == 0) return 1;
+  if (v && strcmp(v, "flow") == 0) return 0;
+  return nc == 4 ? 0 : 1;
+}
+
 template <class E, int B>
 static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
-  constexpr int es = Traits<E>::es;
   MgsStatus *status = w.status.as<MgsStatus>();
   double *orig = w.orig.d();
   const double eps = level_eps(Traits<E>::nc);
   const int sms = num_sms();
+  const int mode = mgs_mode(Traits<E>::nc);
+  if (mode == 0) {
+    constexpr int NT = kMgsThreads;
+    const size_t smem = (size_t)Traits<E>::es * NT * B * sizeof(double);
+    auto kern = k_mgs_flow<E, B, NT>;
+    PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    const int grid = std::min(per_sm * sms, n + 1);
+    if (per_sm > 0 && (n + 1 + grid - 1) / grid <= 64) {
+      w.ready.ensure((size_t)(n + 1) * sizeof(int));
+      PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+      int *ready = w.ready.as<int>();
+      void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
+      count_launch(1);
+      return;
+    }
+  }
+  if (mode <= 1) {
+    int per_sm = 0;
+    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_dataflow<E, B>, kMgsThreads, 0));
+    if (per_sm > 0) {
+      w.ready.ensure((size_t)(n + 1) * sizeof(int));
+      PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+      int *ready = w.ready.as<int>();
+      const int grid = std::min(per_sm * sms, n + 1);
+      void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_mgs_dataflow<E, B>, grid, kMgsThreads, args, 0, st));
+      count_launch(1);
+      return;
+    }
+  }
   k_mgs_orig<E, B><<<std::min(n, sms * 4), kMgsThreads, 0, st>>>(A, m, n, orig);
   PN_CHECK_LAUNCH();
   k_mgs_pivot<E, B><<<1, kMgsThreads, 0, st>>>(A, m, n, 0, orig, eps, Q, R, status);
@@ -241,7 +702,6 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
   }
   PN_CHECK_LAUNCH();
   count_launch(n);
-  (void)es;
 }
 
 template <class E>

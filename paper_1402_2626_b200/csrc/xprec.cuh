@@ -113,6 +113,21 @@ PN_DI F<4> renorm5(double c0, double c1, double c2, double c3, double c4) {
   quick_two_sum(c2, s, s, t3);
   quick_two_sum(c1, s, s, t2);
   quick_two_sum(c0, s, cur, t1);
+  F<4> r;
+  // Common case: the first three steps all leave a nonzero error term, so
+  // every step "advances" and the fourth folds into the last slot
+  // (_eft.py:142-150 with k reaching 3).  Same operations as the general
+  // path below; the branch is warp-uniform on generic data.
+  {
+    double s1, e1, s2, e2, s3, e3;
+    quick_two_sum(cur, t1, s1, e1);
+    quick_two_sum(e1, t2, s2, e2);
+    quick_two_sum(e2, t3, s3, e3);
+    if (e1 != 0.0 && e2 != 0.0 && e3 != 0.0) {
+      r.c[0] = s1; r.c[1] = s2; r.c[2] = s3; r.c[3] = dadd(e3, t4);
+      return r;
+    }
+  }
   double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
   int k = 0;
   const double tv[4] = {t1, t2, t3, t4};
@@ -130,12 +145,15 @@ PN_DI F<4> renorm5(double c0, double c1, double c2, double c3, double c4) {
   o1 = (k == 1) ? cur : o1;
   o2 = (k == 2) ? cur : o2;
   o3 = (k == 3) ? cur : o3;
-  F<4> r;
   r.c[0] = o0; r.c[1] = o1; r.c[2] = o2; r.c[3] = o3;
   return r;
 }
 
-PN_DI F<4> fadd(const F<4> &a, const F<4> &b) {
+#ifndef PN_QD_CALL
+#define PN_QD_CALL static __device__ __noinline__
+#endif
+
+PN_DI F<4> qd_add_body(const F<4> &a, const F<4> &b) {
   double s1, s2, s3, s4, t1, t2, t3, t4;
   two_sum(a.c[0], b.c[0], s1, t1);
   two_sum(a.c[1], b.c[1], s2, t2);
@@ -147,9 +165,7 @@ PN_DI F<4> fadd(const F<4> &a, const F<4> &b) {
   t4 = dadd(dadd(t4, t3), t1);
   return renorm5(s1, s2, s3, s4, t4);
 }
-PN_DI F<4> fsub(const F<4> &a, const F<4> &b) { return fadd(a, fneg(b)); }
-
-PN_DI F<4> fmul(const F<4> &a, const F<4> &b) {
+PN_DI F<4> qd_mul_body(const F<4> &a, const F<4> &b) {
   const double a0 = a.c[0], a1 = a.c[1], a2 = a.c[2], a3 = a.c[3];
   const double b0 = b.c[0], b1 = b.c[1], b2 = b.c[2], b3 = b.c[3];
   double p0, q0, p1, q1, p2, q2, p3, q3, p4, q4, p5, q5;
@@ -194,6 +210,16 @@ PN_DI F<4> fmul(const F<4> &a, const F<4> &b) {
   t1 = dadd(dadd(dadd(t1, u), w), s2);
   return renorm5(p0, p1, s0, t0, t1);
 }
+
+// The quad-double primitives are out-of-line calls by default: a fully
+// inlined complex-qd kernel is >1 MB of SASS and stalls on instruction fetch
+// (ncu: stall_no_inst 35-45%); one shared copy of each primitive fits the
+// instruction cache.
+PN_QD_CALL F<4> qd_add_call(F<4> a, F<4> b) { return qd_add_body(a, b); }
+PN_QD_CALL F<4> qd_mul_call(F<4> a, F<4> b) { return qd_mul_body(a, b); }
+PN_DI F<4> fadd(const F<4> &a, const F<4> &b) { return qd_add_call(a, b); }
+PN_DI F<4> fsub(const F<4> &a, const F<4> &b) { return qd_add_call(a, fneg(b)); }
+PN_DI F<4> fmul(const F<4> &a, const F<4> &b) { return qd_mul_call(a, b); }
 
 // ---- reciprocal / division / sqrt ---------------------------------------
 // recip(b) is the Newton-refined reciprocal of the reference's division;

@@ -186,8 +186,15 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
+@pytest.fixture(params=["flow", "dataflow", "sweeps"])
+def mgs_mode(request, monkeypatch):
+    """Both MGS schedules (persistent dataflow kernel, launch per sweep)."""
+    monkeypatch.setenv("PN_MGS_MODE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name", [n for n in golden_names("mgs_") if "breakdown" not in n])
-def test_least_squares_golden(gpu, name):
+def test_least_squares_golden(gpu, mgs_mode, name):
     from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve, mgs_qr
     from paper_1402_2626_b200.varith import VecContext
     g = golden(name)
@@ -202,7 +209,7 @@ def test_least_squares_golden(gpu, name):
     assert same(f.R, g["R"])
 
 
-def test_breakdown_golden(gpu):
+def test_breakdown_golden(gpu, mgs_mode):
     from paper_1402_2626_b200.mgs import AugmentedMatrix, MgsBreakdownError, mgs_qr
     from paper_1402_2626_b200.varith import VecContext
     g = golden("mgs_breakdown_rdd")
@@ -213,7 +220,7 @@ def test_breakdown_golden(gpu):
 
 
 @pytest.mark.parametrize("lv,m,n", [("cqd", 160, 128), ("cdd", 513, 200), ("rdd", 1030, 64), ("cd", 256, 256)])
-def test_least_squares_vs_oracle(gpu, lv, m, n):
+def test_least_squares_vs_oracle(gpu, mgs_mode, lv, m, n):
     from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
     from paper_1402_2626_b200.varith import VecContext
     L = oracle_level(lv)
@@ -227,6 +234,24 @@ def test_least_squares_vs_oracle(gpu, lv, m, n):
     assert same(res.factors.Q, Q)
     assert same(res.x, x)
     assert res.z == z
+
+
+@pytest.mark.parametrize("lv", ["cdd", "rqd", "cd"])
+def test_breakdown_mid_factorisation_vs_oracle(gpu, mgs_mode, lv):
+    """A dependent column deep in the matrix: every CTA of the dataflow kernel
+    must stop cleanly and report the reference's (k, rkk, threshold)."""
+    from paper_1402_2626_b200.mgs import AugmentedMatrix, MgsBreakdownError, mgs_qr
+    from paper_1402_2626_b200.varith import VecContext
+    L = oracle_level(lv)
+    rng = np.random.default_rng(17)
+    aug = rng.uniform(-1, 1, L.cshape + (300, 201))
+    aug[..., 157] = aug[..., 3] * 0.5  # exact multiple of column 3
+    aug = np.ascontiguousarray(aug)
+    with pytest.raises(oracle.Breakdown) as want:
+        oracle.mgs_qr(L, aug, nthreads=8)
+    with pytest.raises(MgsBreakdownError) as got:
+        mgs_qr(AugmentedMatrix(VecContext(level_from_name(lv)), aug))
+    assert (got.value.k, got.value.rkk, got.value.threshold) == (want.value.k, want.value.rkk, want.value.threshold)
 
 
 def test_singular_back_substitution(gpu):
