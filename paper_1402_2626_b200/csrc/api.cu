@@ -28,7 +28,7 @@ void mgs_factor_device(int nc, int cplx, int m, int n, double *A, double *Q, dou
 }
 
 void backsub_device(int nc, int cplx, int n, const double *R, double *x, MgsWork &w, cudaStream_t st) {
-  PN_REQUIRE(n <= kBacksubThreads * 4, PN_E_ARG, "back substitution supports n <= %d", kBacksubThreads * 4);
+  PN_REQUIRE(n >= 1, PN_E_ARG, "back substitution needs n >= 1");
   w.status.ensure(sizeof(MgsStatus));
   dispatch_level(nc, cplx, [&]<class E>() { backsub_impl<E>(n, R, x, w, st); });
 }

@@ -18,6 +18,8 @@
 // Each CTA handles one column at a time; thread t owns the aligned row block
 // [t*B, t*B+B), so dot products and norms reduce in the reference's
 // canonical pairwise order (block_tree_reduce) and are bit-identical.
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 #include <cstring>
 
@@ -715,11 +717,103 @@ void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStr
   }
 }
 
+// Blocked back substitution over 32-row diagonal blocks, bottom to top
+// (cooperative launch, one grid barrier per block).  Warp 0 of CTA 0 solves
+// the diagonal block (lane l holds row lo+l; x_j is a shuffle broadcast) and
+// then applies the freshly solved x to the next block's rows itself; all other
+// rows above are updated by the rest of the grid, one thread per row.  Every
+// row still receives its subtractions in descending column order, so x is
+// bit-identical to the reference's sequential solve (mgs.py:229-247).
+template <class E, int NT>
+__global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict__ R, int n, double *__restrict__ x,
+                                                        RDiv<Traits<E>::nc> *__restrict__ prep,
+                                                        double *__restrict__ y, int *sing, MgsStatus *status) {
+  namespace cg = cooperative_groups;
+  constexpr int es = Traits<E>::es;
+  cg::grid_group grid = cg::this_grid();
+  if (status->code) return;  // the factorisation failed (uniform for all CTAs)
+  const long long ld = n + 1;
+  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
+  for (int j = gtid; j < n; j += gsize) {
+    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
+    const double *dg = R + ((long long)j * ld + j) * es;
+    bool nz = false;
+#pragma unroll
+    for (int p = 0; p < es; ++p) nz |= dg[p] != 0.0;
+    if (!nz) atomicMax(sing, j);
+    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
+  }
+  grid.sync();
+  if (*(volatile int *)sing >= 0) {
+    if (gtid == 0) {
+      status->k = *sing;
+      status->code = PN_E_SINGULAR;
+    }
+    return;
+  }
+  const bool solver = blockIdx.x == 0 && threadIdx.x < 32;
+  const int lane = threadIdx.x & 31;
+  const int nb = (n + 31) / 32;
+  E yr = ezero<E>();  // solver lane's row of the current diagonal block
+  if (solver) {
+    const int r = (nb - 1) * 32 + lane;
+    if (r < n) yr = eload<E>(y + (long long)r * es);
+  }
+  for (int b = nb - 1; b >= 0; --b) {
+    const int lo = b * 32, hi = min(n, lo + 32);
+    if (solver) {
+      E xl = ezero<E>();
+      for (int j = hi - 1; j >= lo; --j) {
+        const int jl = j - lo;
+        if (lane == jl) xl = ediv_with(yr, eload<E>(R + ((long long)j * ld + j) * es), prep[j]);
+        const E xj = eshfl_idx(xl, jl);
+        if (lane < jl) yr = esub(yr, emul(eload<E>(R + ((long long)j * ld + lo + lane) * es), xj));
+      }
+      if (lo + lane < hi) estore(x + (long long)(lo + lane) * es, xl);
+    }
+    grid.sync();
+    if (b == 0) break;
+    // rows of block b-1 (solver warp) and all rows above it (rest of the grid)
+    if (solver) {
+      const int r = lo - 32 + lane;
+      yr = eload<E>(y + (long long)r * es);
+      for (int j = hi - 1; j >= lo; --j)
+        yr = esub(yr, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+    } else {
+      const int worker = blockIdx.x == 0 ? threadIdx.x - 32 : gtid - 32;
+      const int workers = gsize - 32;
+      for (int r = worker; r < lo - 32; r += workers) {
+        E v = eload<E>(y + (long long)r * es);
+        for (int j = hi - 1; j >= lo; --j)
+          v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+        estore(y + (long long)r * es, v);
+      }
+    }
+  }
+}
+
 template <class E>
 void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st) {
-  constexpr int NT = kBacksubThreads;
   constexpr int es = Traits<E>::es;
   DevBuf prep((size_t)n * Traits<E>::nc * sizeof(double) + 16, st);
+  const char *mode = getenv("PN_BACKSUB_MODE");
+  if (!(mode && strcmp(mode, "single") == 0)) {
+    constexpr int NT = 128;
+    DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
+    DevBuf sbuf(16, st);
+    int *sing = sbuf.as<int>();
+    PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
+    const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
+    RDiv<Traits<E>::nc> *pp = prep.as<RDiv<Traits<E>::nc>>();
+    double *yp = yw.d();
+    MgsStatus *status = w.status.as<MgsStatus>();
+    void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_blocked<E, NT>, grid, NT, args, 0, st));
+    count_launch(1);
+    return;
+  }
+  constexpr int NT = kBacksubThreads;
+  PN_REQUIRE(n <= NT * 4, PN_E_ARG, "single-CTA back substitution supports n <= %d", NT * 4);
   DevBuf xs((size_t)n * es * sizeof(double) + 16, st);
   k_backsub<E, NT><<<1, NT, 0, st>>>(R, n, x, prep.as<RDiv<Traits<E>::nc>>(), xs.as<E>(), w.status.as<MgsStatus>());
   PN_CHECK_LAUNCH();

@@ -435,6 +435,14 @@ template <class E> PN_DI E eshfl_xor(const E &v, int mask) {
   for (int i = 0; i < Traits<E>::es; ++i) d[i] = __shfl_xor_sync(0xffffffffu, s[i], mask);
   return r;
 }
+template <class E> PN_DI E eshfl_idx(const E &v, int src) {
+  E r;
+  const double *s = reinterpret_cast<const double *>(&v);
+  double *d = reinterpret_cast<double *>(&r);
+#pragma unroll
+  for (int i = 0; i < Traits<E>::es; ++i) d[i] = __shfl_sync(0xffffffffu, s[i], src);
+  return r;
+}
 template <class E> PN_DI E eshfl_down(const E &v, int delta) {
   E r;
   const double *s = reinterpret_cast<const double *>(&v);

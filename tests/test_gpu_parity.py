@@ -254,6 +254,27 @@ def test_breakdown_mid_factorisation_vs_oracle(gpu, mgs_mode, lv):
     assert (got.value.k, got.value.rkk, got.value.threshold) == (want.value.k, want.value.rkk, want.value.threshold)
 
 
+@pytest.mark.parametrize("bmode", ["blocked", "single"])
+@pytest.mark.parametrize("lv,n", [("cqd", 77), ("cdd", 1000), ("rd", 33), ("cd", 1500), ("rqd", 64)])
+def test_back_substitution_vs_oracle(gpu, monkeypatch, bmode, lv, n):
+    from paper_1402_2626_b200.mgs import back_substitute
+    from paper_1402_2626_b200.varith import VecContext
+    if bmode == "single" and n > 1024:
+        pytest.skip("single-CTA variant is limited to n <= 1024")
+    monkeypatch.setenv("PN_BACKSUB_MODE", bmode)
+    L = oracle_level(lv)
+    rng = np.random.default_rng(n)
+    Ra = np.zeros(L.cshape + (n + 1, n + 1))
+    Ra[...] = rng.uniform(-1, 1, Ra.shape)
+    Ra.reshape(L.es, n + 1, n + 1)[[i for i in range(L.es) if i % L.nc != 0]] *= 1e-17
+    Ra[..., np.tril_indices(n + 1, -1)[0], np.tril_indices(n + 1, -1)[1]] = 0.0
+    Ra.reshape(L.es, n + 1, n + 1)[0, np.arange(n), np.arange(n)] += 4.0  # well conditioned
+    Ra = np.ascontiguousarray(Ra)
+    ctx = VecContext(level_from_name(lv))
+    got = back_substitute(Ra[..., :n, :n], Ra[..., :n, n], ctx)
+    assert same(got, oracle.back_substitute(L, Ra))
+
+
 def test_singular_back_substitution(gpu):
     from paper_1402_2626_b200.mgs import SingularMatrixError, back_substitute
     from paper_1402_2626_b200.varith import VecContext
