@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpolynewt_b200.so")
+# PN_LIB selects an alternative build (performance experiments only)
+LIB_PATH = os.environ.get("PN_LIB") or os.path.join(_HERE, "lib", "libpolynewt_b200.so")
 
 PN_OK = 0
 PN_E_ARG = 1

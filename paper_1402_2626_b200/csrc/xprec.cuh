@@ -296,6 +296,27 @@ template <int NC> PN_DI C<NC> cmul(const C<NC> &a, const C<NC> &b) {
 }
 template <int NC> PN_DI C<NC> cconj(const C<NC> &a) { return {a.re, fneg(a.im)}; }
 
+#ifndef PN_QD_MODE
+#define PN_QD_MODE 1
+#endif
+#if PN_QD_MODE == 1
+// Complex quad-double ops as single out-of-line units: the four real products
+// of a complex multiply are independent, so inlining them inside one call
+// lets the scheduler interleave them, while each kernel keeps one copy of the
+// code (instruction-cache friendly) and pays one call per 914 FP64 instr.
+PN_QD_CALL C<4> c4_mul_call(C<4> a, C<4> b) {
+  const F<4> t1 = qd_mul_body(a.re, b.re);
+  const F<4> t2 = qd_mul_body(a.im, b.im);
+  const F<4> t3 = qd_mul_body(a.re, b.im);
+  const F<4> t4 = qd_mul_body(a.im, b.re);
+  return {qd_add_body(t1, fneg(t2)), qd_add_body(t3, t4)};
+}
+PN_QD_CALL C<4> c4_add_call(C<4> a, C<4> b) { return {qd_add_body(a.re, b.re), qd_add_body(a.im, b.im)}; }
+template <> PN_DI C<4> cmul<4>(const C<4> &a, const C<4> &b) { return c4_mul_call(a, b); }
+template <> PN_DI C<4> cadd<4>(const C<4> &a, const C<4> &b) { return c4_add_call(a, b); }
+template <> PN_DI C<4> csub<4>(const C<4> &a, const C<4> &b) { return c4_add_call(a, {fneg(b.re), fneg(b.im)}); }
+#endif
+
 // ---------------------------------------------------------------------------
 // generic element interface: E = F<NC> (real level) or C<NC> (complex level)
 
