@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="config C5: number of homotopy start points (use with --dim 256 --terms 256 --base dd)")
+    ap.add_argument("--max-iters", type=int, default=8)
     return ap.parse_args()
 
 
@@ -180,7 +183,8 @@ def build_inputs(args, rank=0):
     from paper_1402_2626_b200.xprec import precision_level
     level = precision_level(args.base, True)
     m = args.rows or args.dim
-    packed = random_sparse_system(args.dim, args.terms, args.k, level, seed=args.seed, m=m)
+    # every rank solves its own system (independent units)
+    packed = random_sparse_system(args.dim, args.terms, args.k, level, seed=args.seed + rank, m=m)
     rng = np.random.default_rng(args.seed + 1)
     x = rng.uniform(0.5, 2.0, level.cshape + (args.dim,)) * rng.choice([-1.0, 1.0], level.cshape + (args.dim,))
     x[:, 1:] = 0.0  # level.from_float values (SURVEY 8(d) random_point)
@@ -271,10 +275,17 @@ def run_ours(args):
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
     elapsed = e0.elapsed_time(e1) / 1e3
+    gather_s = None
     if world > 1:
         t = torch.tensor([elapsed], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(t.item())
+        # the one collective of the batched path: gather every system's x_next
+        g0 = time.perf_counter()
+        gathered = [torch.empty_like(outs["xn"]) for _ in range(world)]
+        torch.distributed.all_gather(gathered, outs["xn"])
+        torch.cuda.synchronize()
+        gather_s = time.perf_counter() - g0
         torch.distributed.barrier()
     sec_step = elapsed / args.steps
     value = world * args.steps / elapsed
@@ -346,6 +357,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk,
             "prepare_s": t_prep,
+            "gather_s": gather_s,
         }
         if cpu:
             out["quality_up_same_precision"] = value / cpu["value"]
@@ -354,10 +366,92 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_batched(args):
+    """Config C5: B independent homotopy Newton runs of one F(dim, terms, k)
+    system sharded across ranks (no collective on the data path), one
+    all_gather of status / iterations / final x at the end."""
+    import torch
+    world, rank, local = dist_setup()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29512", rank=0, world_size=1)
+    from paper_1402_2626_b200 import _lib
+    from paper_1402_2626_b200.batch import gather_batch, homotopy_batch, run_newton_batch, shard_range
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    from paper_1402_2626_b200.generators import random_sparse_system
+    from paper_1402_2626_b200.xprec import precision_level
+
+    level = precision_level(args.base, True)
+    B = args.batch
+    packed = random_sparse_system(args.dim, args.terms, args.k, level, seed=args.seed)
+    rng = np.random.default_rng(args.seed + 7)
+    theta = rng.uniform(0.0, 2.0 * math.pi, (B, args.dim))
+    Z = np.zeros(level.cshape + (B, args.dim))
+    Z[0, 0] = np.cos(theta)
+    Z[1, 0] = np.sin(theta)
+    lo, hi = shard_range(B, world, rank)
+    Zs = np.ascontiguousarray(Z[..., lo:hi, :])
+    t = level.from_float(0.99)
+    system, consts = homotopy_batch(packed, Zs, t)
+    prep = PreparedSystem(system)
+    # warm-up on one start, then the timed shard
+    run_newton_batch(prep, Zs[..., :1, :], consts[..., :1, :], max_iters=1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = run_newton_batch(prep, Zs, consts, max_iters=args.max_iters)
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    elapsed = e0.elapsed_time(e1) / 1e3
+    it_local = int(res.iters.sum())
+    tt = torch.tensor([elapsed, float(it_local)], dtype=torch.float64,
+                      device="cuda" if world > 1 else "cpu")
+    if world > 1:
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tt.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed, total_iters = float(mx[0]), int(sm[1])
+    else:
+        total_iters = it_local
+    g0 = time.perf_counter()
+    full = gather_batch(res, B)
+    gather_s = time.perf_counter() - g0
+    if rank == 0:
+        counts = {name: int((full.status == code).sum()) for code, name in
+                  [(0, "converged"), (1, "max_iters"), (2, "breakdown"), (3, "singular")]}
+        print(json.dumps({
+            "metric": "batched Newton iterations/sec (start-iterations, eval+diff+MGS), config C5",
+            "value": total_iters / elapsed, "unit": "start-iterations/s", "n_gpus": world, "steps": 1,
+            "warmup": 1, "ms_per_step": elapsed * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5: {B} homotopy starts of F({args.dim},{args.terms},{args.k}) complex "
+                                   f"{args.base}, t=0.99, max_iters={args.max_iters}",
+                       "starts": B, "starts_per_gpu": hi - lo, "parallelism": f"start-sharded x{world}",
+                       "collective": "one all_gather (status, iterations, x) after the run"},
+            "status": counts, "mean_iters": float(full.iters.mean()) if B else 0.0,
+            "gather_s": gather_s, "gpu_launches": launches, "clocks": clk}))
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.batch:
+        run_batched(args)
     else:
         run_ours(args)
 

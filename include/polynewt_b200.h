@@ -158,6 +158,20 @@ int pn_least_squares(int nc, int cplx, int32_t m, int32_t n, const double *aug, 
 int pn_newton_step(pn_system *sys, const double *x, double *x_next, double *f, double *dx,
                    double *fmod, double *dxmod, double *xmod, pn_numinfo *info, void *stream);
 
+/* Batched Newton runs (config C5): B independent run_newton calls
+ * (newton.py:106-132) sharing the system's supports and coefficients.
+ * x0, x_out: planes (cshape, B, n).  consts: planes (cshape, B, m) with the
+ * coefficient of polynomial i's constant term for start b (the homotopy
+ * shift of newton.py:135-159, already added to any base constant), or NULL;
+ * with consts every polynomial must have exactly one constant term.
+ * tol <= 0 selects the reference default 10*eps*(1+||x||_inf).
+ * iters[b] = iterations run; status[b] = 0 converged, 1 max_iters reached,
+ * 2 MGS breakdown, 3 singular back substitution. */
+int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters, double tol,
+                    double *x_out, int32_t *iters, int32_t *status, void *stream);
+/* values f(x_b) for a batch of points: x planes (cshape, B, n) -> f planes (cshape, B, m) */
+int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, double *f, void *stream);
+
 /* ---- synthetic inputs -------------------------------------------------------- */
 /* SURVEY 8(d) F(n, T, k, seed, maxexp, m): m polynomials in n variables, T
  * monomials each of k distinct variables (uniform subset), exponents uniform

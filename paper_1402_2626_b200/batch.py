@@ -1,0 +1,188 @@
+"""Batched Newton runs over independent start points
+and their sharding across GPUs.
+
+A batch is B runs of ``run_newton`` (newton.py:106-132) on the homotopy start
+systems ``homotopy_start_system(system, z_b, t)`` (newton.py:135-159): all
+starts share the supports and coefficients and differ only in the constant
+term of each polynomial.  The GPU keeps one resident system and swaps the m
+constants per start (``pn_newton_batch``); results are bit-identical to the
+one-at-a-time path.  Starts are independent units: ``shard_range`` splits
+them across ranks with no collective on the data path, and ``gather_batch``
+collects status, iteration counts and final iterates once at the end
+(NCCL over NVLink on the GPU box, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .evaldiff import PreparedSystem
+from .polyrep import PackedSystem
+from .varith import VecContext
+from .xprec import PrecisionLevel
+
+STATUS = {0: "converged", 1: "max_iters", 2: "breakdown", 3: "singular"}
+
+
+@dataclass
+class BatchResult:
+    x: np.ndarray        # planes cshape + (B, n)
+    iters: np.ndarray    # int32 (B,)
+    status: np.ndarray   # int32 (B,)
+
+
+def shard_range(B: int, world: int, rank: int) -> tuple:
+    """Contiguous block of start indices owned by `rank` (balanced)."""
+    base, extra = divmod(B, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def evaluate_batch(prep: PreparedSystem, X: np.ndarray) -> np.ndarray:
+    """f(x_b) for X planes cshape + (B, n) -> planes cshape + (B, m)."""
+    level = prep.level
+    B = X.shape[-2]
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    F = np.empty(level.cshape + (B, prep.n_eqs))
+    _lib.check(_lib.load().pn_evaldiff_batch(prep.handle, B, _lib.ptr(X), _lib.ptr(F), None))
+    return F
+
+
+def _with_constant_terms(packed: PackedSystem):
+    """Copy of the system in which every polynomial has a constant term (a
+    placeholder 1 where the base has none); returns it and, per polynomial,
+    the index of the base constant monomial or -1."""
+    level = packed.level
+    m = packed.n_eqs
+    ks = np.diff(packed.mon_ptr)
+    base_const = np.full(m, -1, dtype=np.int64)
+    poly_ptr, mon_ptr, cols = [0], [0], []
+    for i in range(m):
+        lo, hi = int(packed.poly_ptr[i]), int(packed.poly_ptr[i + 1])
+        consts = np.nonzero(ks[lo:hi] == 0)[0]
+        if len(consts) > 1:
+            raise ValueError("duplicate constant term")
+        for c in range(lo, hi):
+            mon_ptr.append(mon_ptr[-1] + int(ks[c]))
+            cols.append(c)
+        if len(consts):
+            base_const[i] = lo + int(consts[0])
+        else:
+            mon_ptr.append(mon_ptr[-1])
+            cols.append(-1)
+        poly_ptr.append(len(mon_ptr) - 1)
+    coef = packed.coeffs.reshape(level.es, -1)
+    newc = np.zeros((level.es, len(cols)))
+    for j, c in enumerate(cols):
+        if c >= 0:
+            newc[:, j] = coef[:, c]
+        else:
+            newc[0, j] = 1.0  # placeholder, replaced per start
+    sel = [c for c in cols if c >= 0]
+    var_idx = np.concatenate([packed.var_idx[packed.mon_ptr[c]:packed.mon_ptr[c + 1]] for c in sel]) if sel else \
+        np.zeros(0, np.int32)
+    exps = np.concatenate([packed.exps[packed.mon_ptr[c]:packed.mon_ptr[c + 1]] for c in sel]) if sel else \
+        np.zeros(0, np.int32)
+    out = PackedSystem(level, packed.n_vars, np.asarray(poly_ptr, np.int32), np.asarray(mon_ptr, np.int32),
+                       var_idx.astype(np.int32), exps.astype(np.int32),
+                       np.ascontiguousarray(newc.reshape(level.cshape + (len(cols),))))
+    return out, base_const
+
+
+def homotopy_batch(packed: PackedSystem, Z: np.ndarray, t):
+    """Per-start constants of homotopy_start_system(system, z_b, t) for all b.
+
+    Returns (system_with_constants, consts planes cshape + (B, m)).  The
+    arithmetic (f(z_b), -(t*f), const + shift) runs on the GPU with the
+    reference's operand order."""
+    level = packed.level
+    B = Z.shape[-2]
+    m = packed.n_eqs
+    base_prep = PreparedSystem(packed)
+    F = evaluate_batch(base_prep, Z)                      # cshape + (B, m)
+    Ff = F.reshape(level.cshape + (B * m,))
+    ctx = VecContext(level)
+    if level.cplx and not (hasattr(t, "re") and hasattr(t, "im")):
+        rl = PrecisionLevel(level.base, False)
+        rctx = VecContext(rl)
+        tp = np.repeat(rl.to_planes([t]), B * m, axis=-1)
+        prod = np.stack((rctx.mul(Ff[0], tp), rctx.mul(Ff[1], tp)))
+    else:
+        tp = np.repeat(level.to_planes([t]), B * m, axis=-1)
+        prod = ctx.mul(tp, Ff)
+    shift = (-prod).reshape(level.cshape + (B, m))
+    system, base_const = _with_constant_terms(packed)
+    consts = shift.copy()
+    have = base_const >= 0
+    if have.any():
+        cc = packed.coeffs[..., base_const[have]]                       # cshape + (h,)
+        cc = np.broadcast_to(cc[..., None, :], level.cshape + (B, int(have.sum())))
+        sub = np.ascontiguousarray(shift[..., have])
+        consts[..., have] = ctx.add(np.ascontiguousarray(cc), sub)
+    zero = np.all(consts.reshape(level.es, B, m) == 0.0, axis=0)
+    if zero.any():
+        raise ValueError("a homotopy constant is exactly zero; the reference would drop that term "
+                         "(run those starts individually)")
+    return system, np.ascontiguousarray(consts)
+
+
+def run_newton_batch(prep: PreparedSystem, X0: np.ndarray, consts: np.ndarray | None = None,
+                     max_iters: int = 10, tol: float | None = None) -> BatchResult:
+    """B independent Newton runs on the GPU (pn_newton_batch)."""
+    level = prep.level
+    X0 = np.ascontiguousarray(X0, dtype=np.float64)
+    B = X0.shape[-2]
+    X = np.empty_like(X0)
+    iters = np.zeros(B, np.int32)
+    status = np.zeros(B, np.int32)
+    c = None if consts is None else np.ascontiguousarray(consts, dtype=np.float64)
+    rc = _lib.load().pn_newton_batch(prep.handle, B, _lib.ptr(X0), _lib.ptr(c), max_iters,
+                                     -1.0 if tol is None else float(tol), _lib.ptr(X), _lib.ptr(iters),
+                                     _lib.ptr(status), None)
+    _lib.check(rc)
+    del level
+    return BatchResult(X, iters, status)
+
+
+def gather_batch(shard: BatchResult, B: int, group=None) -> BatchResult:
+    """All-gather the shards of a batch (one collective at the end of the run:
+    NCCL over NVLink on GPUs, gloo on CPU).  Every rank gets the full result."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    lo, hi = shard_range(B, world, rank)
+    assert shard.x.shape[-2] == hi - lo
+    cshape = shard.x.shape[:-2]
+    n = shard.x.shape[-1]
+    width = -(-B // world)  # pad every shard to the same count
+    es = int(np.prod(cshape))
+
+    def pad(a, cols):
+        out = np.zeros(a.shape[:-1] + (width,) if cols is None else (width,) + a.shape[1:], a.dtype)
+        if cols is None:
+            out[..., : a.shape[-1]] = a
+        else:
+            out[: a.shape[0]] = a
+        return out
+    xs = np.moveaxis(shard.x.reshape(es, hi - lo, n), 1, 0)               # (count, es, n)
+    payload = {"x": pad(xs, 1), "iters": pad(shard.iters, None), "status": pad(shard.status, None)}
+    out = {}
+    for key, arr in payload.items():
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        bufs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(bufs, t, group=group)
+        parts = []
+        for r, buf in enumerate(bufs):
+            rlo, rhi = shard_range(B, world, r)
+            a = buf.cpu().numpy()
+            parts.append(a[..., : rhi - rlo] if a.ndim == 1 else a[: rhi - rlo])
+        out[key] = np.concatenate(parts, axis=0 if key == "x" else -1)
+    x = np.moveaxis(out["x"], 0, 1).reshape(cshape + (B, n))
+    return BatchResult(np.ascontiguousarray(x), out["iters"].astype(np.int32), out["status"].astype(np.int32))

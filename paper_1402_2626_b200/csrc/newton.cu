@@ -1,6 +1,10 @@
 // newton.cu -- one Gauss-Newton correction, device resident end to end
 // (newton.py:82-103): f, J at x -> [J | -f] -> MGS least squares -> x + dx,
 // plus the field moduli the host turns into the reference's float norms.
+#include <cmath>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -83,6 +87,179 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
     info->t_solve = ms[1] * 1e-3;
     info->t_update = ms[2] * 1e-3;
   }
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));
+  PN_API_END
+}
+
+// ---------------------------------------------------------------------------
+// Batched Newton runs: B independent run_newton
+// calls (newton.py:106-132) on one system whose constant terms differ per
+// start (the homotopy shift of newton.py:144-158).  The system's supports and
+// coefficients stay resident; per start only the m constant coefficients
+// and x change.  Starts are independent units, so multi-GPU runs shard them
+// with no collective on the data path (bench.py gathers the results once).
+
+namespace {
+
+template <class E>
+__global__ void k_scatter_consts(int m, const int32_t *__restrict__ cpos, const double *__restrict__ src,
+                                 double *__restrict__ coeff) {
+  constexpr int es = Traits<E>::es;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) estore(coeff + (long long)cpos[i] * es, eload<E>(src + (long long)i * es));
+}
+
+// Python's math.fsum (CPython's msum with the half-even fix-up): the float()
+// of a quad double (xprec.py:261-262) used by the convergence test.
+double host_fsum(const double *v, int n) {
+  double p[16];
+  int np = 0;
+  for (int t = 0; t < n; ++t) {
+    double x = v[t];
+    int i = 0;
+    for (int j = 0; j < np; ++j) {
+      double y = p[j];
+      if (std::fabs(x) < std::fabs(y)) std::swap(x, y);
+      const double hi = x + y, yr = hi - x, lo = y - yr;
+      if (lo != 0.0) p[i++] = lo;
+      x = hi;
+    }
+    np = i;
+    if (x != 0.0) p[np++] = x;
+  }
+  double hi = 0.0, lo = 0.0;
+  if (np > 0) {
+    hi = p[--np];
+    while (np > 0) {
+      const double x = hi, y = p[--np];
+      hi = x + y;
+      const double yr = hi - x;
+      lo = y - yr;
+      if (lo != 0.0) break;
+    }
+    if (np > 0 && ((lo < 0.0 && p[np - 1] < 0.0) || (lo > 0.0 && p[np - 1] > 0.0))) {
+      const double y = lo * 2.0, x = hi + y, yr = x - hi;
+      if (y == yr) hi = x;
+    }
+  }
+  return hi;
+}
+
+// max over float(modulus(v)) (newton.py:33-34) from AoS real moduli
+double host_inf_norm(const std::vector<double> &mod, int nc, int len) {
+  double best = 0.0;
+  for (int i = 0; i < len; ++i) {
+    const double *c = mod.data() + (size_t)i * nc;
+    const double v = nc == 1 ? c[0] : nc == 2 ? c[0] + c[1] : host_fsum(c, 4);
+    if (v > best) best = v;
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
+                               double tol, double *x_out, int32_t *iters, int32_t *status, void *stream) {
+  PN_API_BEGIN
+  PN_REQUIRE(sys && x0 && x_out && iters && status && B >= 0 && max_iters >= 1, PN_E_ARG,
+             "pn_newton_batch: bad arguments");
+  const int m = sys->m, n = sys->n, es = sys->es, nc = sys->nc, cplx = sys->cplx;
+  PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t ebytes = (size_t)es * sizeof(double);
+  // constant monomial of every polynomial (canonical order puts it first)
+  DevBuf cpos_d(sizeof(int32_t) * (m + 1), st);
+  if (consts) {
+    std::vector<int32_t> mon_ptr(sys->M + 1), cpos(m, -1);
+    PN_CHECK_CUDA(cudaMemcpy(mon_ptr.data(), sys->d_mon_ptr, sizeof(int32_t) * (sys->M + 1), cudaMemcpyDeviceToHost));
+    // poly boundaries come from the value segments (seg_ptr[0..m])
+    std::vector<int64_t> seg(m + 1);
+    PN_CHECK_CUDA(cudaMemcpy(seg.data(), sys->d_seg_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) {
+      for (int64_t c = seg[i]; c < seg[i + 1]; ++c)
+        if (mon_ptr[c + 1] == mon_ptr[c]) {
+          PN_REQUIRE(cpos[i] < 0, PN_E_ARG, "polynomial %d has more than one constant term", i);
+          cpos[i] = (int32_t)c;
+        }
+      PN_REQUIRE(cpos[i] >= 0, PN_E_ARG, "per-start constants need a constant term in every polynomial (row %d)", i);
+    }
+    PN_CHECK_CUDA(cudaMemcpyAsync(cpos_d.p, cpos.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  }
+  DevIn xin(x0, (size_t)B * n * es, st);
+  DevIn cin(consts, consts ? (size_t)B * m * es : 0, st);
+  DevBuf xa_all((size_t)B * n * ebytes + 16, st), ca_all(consts ? (size_t)B * m * ebytes + 16 : 16, st);
+  if (B) planes_to_aos(es, B * n, xin.d, xa_all.d(), st);
+  if (consts && B) planes_to_aos(es, B * m, cin.d, ca_all.d(), st);
+  sys->Abuf.ensure((size_t)m * (n + 1) * ebytes);
+  sys->fbuf.ensure((size_t)m * ebytes);
+  sys->vbuf.ensure((size_t)m * n * ebytes);
+  sys->Rbuf.ensure((size_t)(n + 1) * (n + 1) * ebytes);
+  sys->xsol.ensure((size_t)2 * n * ebytes);
+  double *A = sys->Abuf.d(), *fa = sys->fbuf.d(), *Q = sys->vbuf.d(), *R = sys->Rbuf.d();
+  double *dxa = sys->xsol.d(), *xn = dxa + (size_t)n * es;
+  DevBuf mod((size_t)2 * n * nc * sizeof(double) + 16, st);
+  std::vector<double> hmod((size_t)2 * n * nc);
+  const double eps = nc == 1 ? 0x1p-53 : nc == 2 ? 0x1p-104 : 0x1p-209;
+  for (int64_t b = 0; b < B; ++b) {
+    double *xb = xa_all.d() + (size_t)b * n * es;
+    if (consts) {
+      dispatch_level(nc, cplx, [&]<class E>() {
+        k_scatter_consts<E><<<(m + 127) / 128, 128, 0, st>>>(m, cpos_d.as<int32_t>(),
+                                                             ca_all.d() + (size_t)b * m * es, sys->d_coeff);
+      });
+      PN_CHECK_LAUNCH();
+      count_launch(1);
+    }
+    int it = 0, stat = 1;
+    for (it = 1; it <= max_iters; ++it) {
+      evaldiff_device(sys, xb, fa, A, m, n, st);
+      mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, st);
+      backsub_device(nc, cplx, n, R, dxa, sys->mgs, st);
+      vec_op_aos(nc, cplx, PN_OP_ADD, n, xb, dxa, xn, st);
+      vec_op_aos(nc, cplx, PN_OP_MODULUS, n, dxa, nullptr, mod.d(), st);
+      vec_op_aos(nc, cplx, PN_OP_MODULUS, n, xn, nullptr, mod.d() + (size_t)n * nc, st);
+      const int rc = mgs_read_status(sys->mgs, nullptr, st);
+      if (rc) {
+        stat = rc == PN_E_BREAKDOWN ? 2 : 3;
+        break;
+      }
+      PN_CHECK_CUDA(cudaMemcpyAsync(xb, xn, (size_t)n * ebytes, cudaMemcpyDeviceToDevice, st));
+      PN_CHECK_CUDA(cudaMemcpyAsync(hmod.data(), mod.d(), hmod.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      PN_CHECK_CUDA(cudaStreamSynchronize(st));
+      const double dxn = host_inf_norm(hmod, nc, n);
+      std::vector<double> xm(hmod.begin() + (size_t)n * nc, hmod.end());
+      const double t = tol > 0.0 ? tol : 10.0 * eps * (1.0 + host_inf_norm(xm, nc, n));
+      if (dxn <= t) {
+        stat = 0;
+        break;
+      }
+    }
+    iters[b] = it > max_iters ? max_iters : it;
+    status[b] = stat;
+  }
+  DevOut xo(x_out, (size_t)B * n * es, st);
+  if (B) aos_to_planes(es, B * n, xa_all.d(), xo.d, st);
+  xo.finish(st);
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));
+  PN_API_END
+}
+
+// values f(x_b) of a batch of points (planes (cshape, B, n) -> (cshape, B, m))
+extern "C" int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, double *f, void *stream) {
+  PN_API_BEGIN
+  PN_REQUIRE(sys && x && f && B >= 0, PN_E_ARG, "pn_evaldiff_batch: bad arguments");
+  const int m = sys->m, n = sys->n, es = sys->es;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t ebytes = (size_t)es * sizeof(double);
+  DevIn xin(x, (size_t)B * n * es, st);
+  DevBuf xa((size_t)B * n * ebytes + 16, st), fa((size_t)B * m * ebytes + 16, st);
+  if (B) planes_to_aos(es, B * n, xin.d, xa.d(), st);
+  sys->Abuf.ensure((size_t)std::max(m, 1) * (n + 1) * ebytes);
+  for (int64_t b = 0; b < B; ++b)
+    evaldiff_device(sys, xa.d() + (size_t)b * n * es, fa.d() + (size_t)b * m * es, sys->Abuf.d(), m, -1, st);
+  DevOut fo(f, (size_t)B * m * es, st);
+  if (B) aos_to_planes(es, B * m, fa.d(), fo.d, st);
+  fo.finish(st);
   PN_CHECK_CUDA(cudaStreamSynchronize(st));
   PN_API_END
 }

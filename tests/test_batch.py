@@ -1,0 +1,108 @@
+"""Batched Newton runs (config C5): sharding/gather host logic on CPU with a
+world-size-2 gloo group, and GPU parity of pn_newton_batch against the
+one-start-at-a-time path and the reference goldens."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden, level_from_name, same
+
+
+def test_shard_range_partitions_every_size():
+    from paper_1402_2626_b200.batch import shard_range
+    for B in (0, 1, 7, 8, 8192, 8193):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(B, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _gather_worker(rank, world, port, B, out_dir):
+    import torch.distributed as dist
+    from paper_1402_2626_b200.batch import BatchResult, gather_batch, shard_range
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    lo, hi = shard_range(B, world, rank)
+    cnt = hi - lo
+    # deterministic stand-in for per-start results: values encode (start, slot)
+    x = np.zeros((2, 2, cnt, 5))
+    for b in range(cnt):
+        x[..., b, :] = (lo + b) * 100 + np.arange(5)
+    shard = BatchResult(x, np.arange(lo, hi, dtype=np.int32) % 7, (np.arange(lo, hi) % 3).astype(np.int32))
+    full = gather_batch(shard, B)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), x=full.x, iters=full.iters, status=full.status)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [9, 16])
+def test_gather_batch_gloo_world2(tmp_path, B):
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_gather_worker, args=(2, port, B, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        d = np.load(tmp_path / f"r{r}.npz")
+        assert d["x"].shape == (2, 2, B, 5)
+        for b in range(B):
+            assert np.array_equal(d["x"][..., b, :], np.broadcast_to(b * 100 + np.arange(5), (2, 2, 5)))
+        assert np.array_equal(d["iters"], np.arange(B) % 7)
+        assert np.array_equal(d["status"], np.arange(B) % 3)
+
+
+# -- GPU ---------------------------------------------------------------------------------
+
+def _packed(g, prefix=""):
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    level = level_from_name(str(g["level"]))
+    return PackedSystem(level, int(g["n_vars"]), g[prefix + "poly_ptr"].astype(np.int32),
+                        g[prefix + "mon_ptr"].astype(np.int32), g[prefix + "var_idx"].astype(np.int32),
+                        g[prefix + "exps"].astype(np.int32), np.ascontiguousarray(g[prefix + "coeffs"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["newton_homotopy_cdd", "newton_homotopy_cqd", "newton_homotopy_cd",
+                                  "newton_cyclic8_cdd"])
+def test_batch_reproduces_reference_run(gpu, name):
+    """B=1 batch on the golden homotopy case == the reference's run_newton."""
+    from paper_1402_2626_b200.batch import homotopy_batch, run_newton_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    g = golden(name)
+    p = _packed(g)
+    level = p.level
+    t = level.from_planes(g["t"])[0]
+    Z = np.ascontiguousarray(g["z"][..., None, :])
+    system, consts = homotopy_batch(p, Z, t)
+    iters = str(g["trace"]).count("\n")
+    res = run_newton_batch(PreparedSystem(system), Z, consts, max_iters=iters)
+    assert same(res.x[..., 0, :], g["x_final"])
+    assert res.iters[0] == iters
+    assert res.status[0] == (0 if bool(g["converged"]) else 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lv", ["cdd", "cd", "cqd"])
+def test_batch_matches_single_runs(gpu, lv):
+    from paper_1402_2626_b200.batch import homotopy_batch, run_newton_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    from paper_1402_2626_b200.generators import random_sparse_system, random_unit_point
+    from paper_1402_2626_b200.newton import NewtonConfig, homotopy_start_system, run_newton
+    level = level_from_name(lv)
+    p = random_sparse_system(16, 8, 4, level, seed=31, maxexp=2)
+    B = 5
+    Z = np.stack([level.to_planes(random_unit_point(16, 100 + b, level)) for b in range(B)], axis=-2)
+    t = level.from_float(0.99)
+    system, consts = homotopy_batch(p, Z, t)
+    res = run_newton_batch(PreparedSystem(system), Z, consts, max_iters=8)
+    for b in range(B):
+        single = homotopy_start_system(p, np.ascontiguousarray(Z[..., b, :]), t)
+        tr = run_newton(single, np.ascontiguousarray(Z[..., b, :]), NewtonConfig(level=level, max_iters=8))
+        assert same(res.x[..., b, :], level.to_planes(tr.x)), b
+        assert res.iters[b] == len(tr.entries)
+        assert res.status[b] == (0 if tr.converged else 1)
