@@ -28,13 +28,23 @@
 
 namespace pn {
 
+// Batched evaluation (config C5): blockIdx.y selects a batch slot; each slot
+// has its own point, power table, contribution buffer, f and [J | -f].  The
+// single-system path uses one slot with zero strides.
+__device__ __forceinline__ long long bslot(const BView &v) {
+  return v.slots ? (long long)v.slots[blockIdx.y] : (long long)blockIdx.y;
+}
+
 // ---------------------------------------------------------------------------
 // K0
 
 template <class E>
 __global__ void k_power_table(int n, const double *__restrict__ x, const int32_t *__restrict__ toff,
-                              const int32_t *__restrict__ tdeg, double *__restrict__ table) {
+                              const int32_t *__restrict__ tdeg, double *__restrict__ table, BView bv) {
   constexpr int es = Traits<E>::es;
+  const long long b = bslot(bv);
+  x += b * bv.x;
+  table += b * bv.t;
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n) return;
   const int deg = tdeg[v];
@@ -57,8 +67,11 @@ __global__ void k_mono_small(const int32_t *__restrict__ list, long long count, 
                              const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
                              const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                              const double *__restrict__ table, const int32_t *__restrict__ toff,
-                             double *__restrict__ contrib) {
+                             double *__restrict__ contrib, BView bv) {
   constexpr int es = Traits<E>::es;
+  const long long b = bslot(bv);
+  table += b * bv.t;
+  contrib += b * bv.c;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < count;
        g += (long long)gridDim.x * blockDim.x) {
     const int c = list[g];
@@ -110,8 +123,15 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
                                                   const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
                                                   const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                                                   const double *__restrict__ x, const double *__restrict__ table,
-                                                  const int32_t *__restrict__ toff, double *__restrict__ contrib) {
+                                                  const int32_t *__restrict__ toff, double *__restrict__ contrib,
+                                                  BView bv) {
   constexpr int es = Traits<E>::es;
+  {
+    const long long b = bslot(bv);
+    x += b * bv.x;
+    table += b * bv.t;
+    contrib += b * bv.c;
+  }
   constexpr int SL = BASE / G;            // slots per lane
   constexpr int NLOC = Log2<SL>::value;   // lane-local levels above the slots
   constexpr int NX = Log2<G>::value;      // butterfly levels
@@ -234,8 +254,15 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
                                                    const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
                                                    const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                                                    const double *__restrict__ x, const double *__restrict__ table,
-                                                   const int32_t *__restrict__ toff, double *__restrict__ contrib) {
+                                                   const int32_t *__restrict__ toff, double *__restrict__ contrib,
+                                                   BView bv) {
   constexpr int es = Traits<E>::es;
+  {
+    const long long b = bslot(bv);
+    x += b * bv.x;
+    table += b * bv.t;
+    contrib += b * bv.c;
+  }
   extern __shared__ __align__(16) double smem[];
   E *lvl = reinterpret_cast<E *>(smem);  // levels back to back: 2*BASE entries
   __shared__ E s_scale;
@@ -314,8 +341,14 @@ template <class E>
 __global__ void __launch_bounds__(128) k_segments(long long nseg_total, int m, const int64_t *__restrict__ seg_ptr,
                                                   const int64_t *__restrict__ seg_out,
                                                   const double *__restrict__ contrib, double *__restrict__ f,
-                                                  double *__restrict__ A, long long negf_off) {
+                                                  double *__restrict__ A, long long negf_off, BView bv) {
   constexpr int es = Traits<E>::es;
+  {
+    const long long b = bslot(bv);
+    contrib += b * bv.c;
+    if (f) f += b * bv.f;
+    A += b * bv.a;
+  }
   E stk[32];
   for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg_total;
        s += (long long)gridDim.x * blockDim.x) {
@@ -352,48 +385,67 @@ template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8
 template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
 
 template <class E, int BASE>
-static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double *x, double *contrib,
-                        cudaStream_t st) {
+static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double *x, const double *table,
+                        double *contrib, int nb, const BView &bv, cudaStream_t st) {
   constexpr int G = TreeG<E>::value < BASE ? TreeG<E>::value : BASE;
   constexpr int NT = 128;
   const long long threads = b.count * G;
-  const int grid = (int)((threads + NT - 1) / NT);
+  const dim3 grid((unsigned)((threads + NT - 1) / NT), (unsigned)nb);
   k_mono_tree<E, BASE, G, NT><<<grid, NT, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,
-                                                   sys->d_dst, sys->d_coeff, x, sys->table.d(), sys->d_toff,
-                                                   contrib);
+                                                   sys->d_dst, sys->d_coeff, x, table, sys->d_toff, contrib, bv);
   PN_CHECK_LAUNCH();
   count_launch(1);
 }
 
+// per-start constant terms (homotopy shifts, newton.py:144-158): after the
+// k <= 1 kernel has written every constant monomial's value, slot b's
+// constant of polynomial i is replaced by consts[b][i]
 template <class E>
-void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
-                          cudaStream_t st) {
+__global__ void k_scatter_consts_batch(int m, const int32_t *__restrict__ cpos, const double *__restrict__ consts,
+                                       long long cstride, double *__restrict__ contrib, BView bv) {
   constexpr int es = Traits<E>::es;
-  const long long M = sys->M, nnz = sys->nnz;
-  PN_REQUIRE(ldA == sys->m, PN_E_ARG, "internal: Jacobian leading dimension must equal m");
-  sys->contrib.ensure((size_t)(M + nnz) * es * sizeof(double) + 16);
-  sys->table.ensure((size_t)(sys->table_len > 0 ? sys->table_len : 1) * es * sizeof(double));
-  double *contrib = sys->contrib.d();
+  const long long b = bslot(bv);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) estore(contrib + b * bv.c + (long long)cpos[i] * es, eload<E>(consts + b * cstride + (long long)i * es));
+}
+
+// zero the Jacobian columns of every slot (absent entries are exact zeros,
+// evaldiff.py:262); column n (-f) is fully written by k_segments
+template <class E>
+__global__ void k_zero_jac(long long count, double *__restrict__ A, BView bv) {
+  double2 *a = reinterpret_cast<double2 *>(A + bslot(bv) * bv.a);
+  const long long n2 = count * Traits<E>::es / 2;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x)
+    a[i] = make_double2(0.0, 0.0);
+}
+
+// the evaluation pipeline for nb slots (nb = 1, zero strides: one system)
+template <class E>
+static void evaldiff_run(pn_system *sys, const double *x, double *table, double *contrib, double *f, double *A,
+                         long long ldA, int negf_col, int nb, const BView &bv, const int32_t *cpos,
+                         const double *consts, long long cstride, cudaStream_t st) {
+  constexpr int es = Traits<E>::es;
+  if (nb <= 0) return;
   if (sys->table_len > 0) {
-    k_power_table<E><<<(sys->n + 127) / 128, 128, 0, st>>>(sys->n, x, sys->d_toff, sys->d_tdeg, sys->table.d());
+    k_power_table<E><<<dim3((sys->n + 127) / 128, nb), 128, 0, st>>>(sys->n, x, sys->d_toff, sys->d_tdeg, table, bv);
     PN_CHECK_LAUNCH();
     count_launch(1);
   }
   for (const auto &b : sys->buckets) {
     if (b.count == 0) continue;
     if (b.kind == 0) {
-      const int grid = (int)std::min<long long>((b.count + 127) / 128, (long long)num_sms() * 16);
-      k_mono_small<E><<<grid, 128, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp, sys->d_dst,
-                                            sys->d_coeff, sys->table.d(), sys->d_toff, contrib);
+      const int gx = (int)std::min<long long>((b.count + 127) / 128, std::max(1LL, (long long)num_sms() * 16 / nb));
+      k_mono_small<E><<<dim3(gx, nb), 128, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,
+                                                    sys->d_dst, sys->d_coeff, table, sys->d_toff, contrib, bv);
       PN_CHECK_LAUNCH();
       count_launch(1);
     } else if (b.kind == 1) {
       switch (b.base) {
-        case 2: launch_tree<E, 2>(b, sys, x, contrib, st); break;
-        case 4: launch_tree<E, 4>(b, sys, x, contrib, st); break;
-        case 8: launch_tree<E, 8>(b, sys, x, contrib, st); break;
-        case 16: launch_tree<E, 16>(b, sys, x, contrib, st); break;
-        case 32: launch_tree<E, 32>(b, sys, x, contrib, st); break;
+        case 2: launch_tree<E, 2>(b, sys, x, table, contrib, nb, bv, st); break;
+        case 4: launch_tree<E, 4>(b, sys, x, table, contrib, nb, bv, st); break;
+        case 8: launch_tree<E, 8>(b, sys, x, table, contrib, nb, bv, st); break;
+        case 16: launch_tree<E, 16>(b, sys, x, table, contrib, nb, bv, st); break;
+        case 32: launch_tree<E, 32>(b, sys, x, table, contrib, nb, bv, st); break;
         default: PN_REQUIRE(false, PN_E_ARG, "internal: bad bucket base %d", b.base);
       }
     } else {
@@ -405,23 +457,56 @@ void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long l
       constexpr int NT = 256;
       PN_CHECK_CUDA(cudaFuncSetAttribute(k_mono_large<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-      const int grid = (int)std::min<long long>(b.count, (long long)num_sms() * 8);
-      k_mono_large<E, NT><<<grid, NT, smem, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,
-                                                  sys->d_dst, sys->d_coeff, x, sys->table.d(), sys->d_toff, contrib);
+      const int gx = (int)std::min<long long>(b.count, std::max(1LL, (long long)num_sms() * 8 / nb));
+      k_mono_large<E, NT><<<dim3(gx, nb), NT, smem, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var,
+                                                          sys->d_exp, sys->d_dst, sys->d_coeff, x, table,
+                                                          sys->d_toff, contrib, bv);
       PN_CHECK_LAUNCH();
       count_launch(1);
     }
   }
-  // dense Jacobian: absent entries are exact zeros (evaldiff.py:262)
-  PN_CHECK_CUDA(cudaMemsetAsync(A, 0, (size_t)sys->n * ldA * es * sizeof(double), st));
-  const long long total = sys->m + sys->nseg;
-  if (total > 0) {
-    const int grid = (int)std::min<long long>((total + 127) / 128, (long long)num_sms() * 32);
-    k_segments<E><<<grid, 128, 0, st>>>(total, sys->m, sys->d_seg_ptr, sys->d_seg_out, contrib, f, A,
-                                        negf_col >= 0 ? (long long)negf_col * ldA : -1);
+  if (consts) {
+    k_scatter_consts_batch<E><<<dim3((sys->m + 127) / 128, nb), 128, 0, st>>>(sys->m, cpos, consts, cstride, contrib,
+                                                                               bv);
     PN_CHECK_LAUNCH();
     count_launch(1);
   }
+  // dense Jacobian: absent entries are exact zeros (evaldiff.py:262)
+  if (nb == 1 && !bv.slots) {
+    PN_CHECK_CUDA(cudaMemsetAsync(A, 0, (size_t)sys->n * ldA * es * sizeof(double), st));
+  } else {
+    const long long cnt = (long long)sys->n * ldA;
+    const int gx = (int)std::min<long long>((cnt * es / 2 + 255) / 256, std::max(1LL, (long long)num_sms() * 8 / nb));
+    k_zero_jac<E><<<dim3(gx, nb), 256, 0, st>>>(cnt, A, bv);
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+  }
+  const long long total = sys->m + sys->nseg;
+  if (total > 0) {
+    const int gx = (int)std::min<long long>((total + 127) / 128, std::max(1LL, (long long)num_sms() * 32 / nb));
+    k_segments<E><<<dim3(gx, nb), 128, 0, st>>>(total, sys->m, sys->d_seg_ptr, sys->d_seg_out, contrib, f, A,
+                                                negf_col >= 0 ? (long long)negf_col * ldA : -1, bv);
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+  }
+}
+
+template <class E>
+void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
+                   cudaStream_t st) {
+  constexpr int es = Traits<E>::es;
+  PN_REQUIRE(ldA == sys->m, PN_E_ARG, "internal: Jacobian leading dimension must equal m");
+  sys->contrib.ensure((size_t)(sys->M + sys->nnz) * es * sizeof(double) + 16);
+  sys->table.ensure((size_t)(sys->table_len > 0 ? sys->table_len : 1) * es * sizeof(double));
+  const BView bv{nullptr, 0, 0, 0, 0, 0};
+  evaldiff_run<E>(sys, x, sys->table.d(), sys->contrib.d(), f, A, ldA, negf_col, 1, bv, nullptr, nullptr, 0, st);
+}
+
+template <class E>
+void evaldiff_batch_impl(pn_system *sys, int nb, const BView &bv, const double *x, double *table, double *contrib,
+                         double *f, double *A, int negf_col, const int32_t *cpos, const double *consts,
+                         long long cstride, cudaStream_t st) {
+  evaldiff_run<E>(sys, x, table, contrib, f, A, sys->m, negf_col, nb, bv, cpos, consts, cstride, st);
 }
 
 // one translation unit per precision level (see Makefile): explicit
@@ -429,6 +514,9 @@ void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long l
 #ifdef PN_NC
 template void evaldiff_impl<PnLevel>(pn_system *, const double *, double *, double *, long long, int,
                                       cudaStream_t);
+template void evaldiff_batch_impl<PnLevel>(pn_system *, int, const BView &, const double *, double *, double *,
+                                           double *, double *, int, const int32_t *, const double *, long long,
+                                           cudaStream_t);
 #endif
 
 }  // namespace pn

@@ -11,6 +11,14 @@
 
 namespace pn {
 
+// batch view of the evaluation kernels: slot b = slots[blockIdx.y] (or
+// blockIdx.y) works on x + b*x, table + b*t, contrib + b*c, A + b*a, f + b*f
+// (strides in doubles)
+struct BView {
+  const int32_t *slots;
+  long long x, t, c, a, f;
+};
+
 void set_error(const char *fmt, ...);
 void count_launch(int n);
 
@@ -180,6 +188,14 @@ void evaldiff_device(pn_system *sys, const double *x, double *f, double *A, long
 template <class E>
 void evaldiff_impl(pn_system *sys, const double *x, double *f, double *A, long long ldA, int negf_col,
                    cudaStream_t st);
+template <class E>
+void evaldiff_batch_impl(pn_system *sys, int nb, const BView &bv, const double *x, double *table, double *contrib,
+                         double *f, double *A, int negf_col, const int32_t *cpos, const double *consts,
+                         long long cstride, cudaStream_t st);
+template <class E>
+void solve_batch_impl(int nb, const int32_t *slots, int m, int n, double *A, long long As, double *Q, long long Qs,
+                      double *R, long long Rs, double *x, long long xs, double *dx, double tol, int32_t *flags,
+                      cudaStream_t st);
 template <class E>
 void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st);
 template <class E>

@@ -2,6 +2,8 @@
 // (newton.py:82-103): f, J at x -> [J | -f] -> MGS least squares -> x + dx,
 // plus the field moduli the host turns into the reference's float norms.
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <utility>
 #include <vector>
 
@@ -158,33 +160,13 @@ double host_inf_norm(const std::vector<double> &mod, int nc, int len) {
 
 }  // namespace
 
-extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
-                               double tol, double *x_out, int32_t *iters, int32_t *status, void *stream) {
-  PN_API_BEGIN
+static void newton_batch_serial(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
+                                double tol, double *x_out, int32_t *iters, int32_t *status, cudaStream_t st,
+                                const DevBuf &cpos_d) {
   PN_REQUIRE(sys && x0 && x_out && iters && status && B >= 0 && max_iters >= 1, PN_E_ARG,
              "pn_newton_batch: bad arguments");
   const int m = sys->m, n = sys->n, es = sys->es, nc = sys->nc, cplx = sys->cplx;
-  PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
-  cudaStream_t st = (cudaStream_t)stream;
   const size_t ebytes = (size_t)es * sizeof(double);
-  // constant monomial of every polynomial (canonical order puts it first)
-  DevBuf cpos_d(sizeof(int32_t) * (m + 1), st);
-  if (consts) {
-    std::vector<int32_t> mon_ptr(sys->M + 1), cpos(m, -1);
-    PN_CHECK_CUDA(cudaMemcpy(mon_ptr.data(), sys->d_mon_ptr, sizeof(int32_t) * (sys->M + 1), cudaMemcpyDeviceToHost));
-    // poly boundaries come from the value segments (seg_ptr[0..m])
-    std::vector<int64_t> seg(m + 1);
-    PN_CHECK_CUDA(cudaMemcpy(seg.data(), sys->d_seg_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < m; ++i) {
-      for (int64_t c = seg[i]; c < seg[i + 1]; ++c)
-        if (mon_ptr[c + 1] == mon_ptr[c]) {
-          PN_REQUIRE(cpos[i] < 0, PN_E_ARG, "polynomial %d has more than one constant term", i);
-          cpos[i] = (int32_t)c;
-        }
-      PN_REQUIRE(cpos[i] >= 0, PN_E_ARG, "per-start constants need a constant term in every polynomial (row %d)", i);
-    }
-    PN_CHECK_CUDA(cudaMemcpyAsync(cpos_d.p, cpos.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-  }
   DevIn xin(x0, (size_t)B * n * es, st);
   DevIn cin(consts, consts ? (size_t)B * m * es : 0, st);
   DevBuf xa_all((size_t)B * n * ebytes + 16, st), ca_all(consts ? (size_t)B * m * ebytes + 16 : 16, st);
@@ -241,10 +223,165 @@ extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, cons
   if (B) aos_to_planes(es, B * n, xa_all.d(), xo.d, st);
   xo.finish(st);
   PN_CHECK_CUDA(cudaStreamSynchronize(st));
+}
+
+
+// position of every polynomial's constant monomial in canonical order
+static void constant_positions(pn_system *sys, DevBuf &cpos_d, cudaStream_t st) {
+  const int m = sys->m;
+  std::vector<int32_t> mon_ptr(sys->M + 1), cpos(m, -1);
+  PN_CHECK_CUDA(cudaMemcpy(mon_ptr.data(), sys->d_mon_ptr, sizeof(int32_t) * (sys->M + 1), cudaMemcpyDeviceToHost));
+  // poly boundaries come from the value segments (seg_ptr[0..m])
+  std::vector<int64_t> seg(m + 1);
+  PN_CHECK_CUDA(cudaMemcpy(seg.data(), sys->d_seg_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < m; ++i) {
+    for (int64_t c = seg[i]; c < seg[i + 1]; ++c)
+      if (mon_ptr[c + 1] == mon_ptr[c]) {
+        PN_REQUIRE(cpos[i] < 0, PN_E_ARG, "polynomial %d has more than one constant term", i);
+        cpos[i] = (int32_t)c;
+      }
+    PN_REQUIRE(cpos[i] >= 0, PN_E_ARG, "per-start constants need a constant term in every polynomial (row %d)", i);
+  }
+  PN_CHECK_CUDA(cudaMemcpyAsync(cpos_d.p, cpos.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));
+}
+
+// slots of a batched run: per-slot device state, all strides in doubles
+struct BatchSlots {
+  int W = 0;
+  long long xs = 0, ts = 0, cs = 0, as = 0, qs = 0, rs = 0, ks = 0;
+  DevBuf x, dx, table, contrib, A, Q, R, k, flags, list;
+};
+
+static long long batch_slot_doubles(const pn_system *sys) {
+  const long long es = sys->es, m = sys->m, n = sys->n;
+  return (sys->M + sys->nnz) * es + std::max(sys->table_len, 1LL) * es + m * (n + 1) * es + m * n * es +
+         (n + 1) * (n + 1) * es + 2 * n * es + m * es;
+}
+
+static int batch_width(const pn_system *sys, int64_t B) {
+  size_t fr = 0, tot = 0;
+  PN_CHECK_CUDA(cudaMemGetInfo(&fr, &tot));
+  const double per = (double)batch_slot_doubles(sys) * sizeof(double);
+  long long W = std::min<long long>(B, 4LL * num_sms());
+  W = std::min<long long>(W, (long long)(0.6 * (double)fr / per));
+  if (const char *v = getenv("PN_BATCH_SLOTS")) W = std::min<long long>(B, std::max(1, atoi(v)));
+  PN_REQUIRE(W >= 1 || B == 0, PN_E_NOMEM, "not enough device memory for one batch slot (%.0f MB)", per / 1e6);
+  return (int)W;
+}
+
+static void batch_alloc(pn_system *sys, BatchSlots &s, int W, cudaStream_t st) {
+  const long long es = sys->es, m = sys->m, n = sys->n;
+  s.W = W;
+  s.xs = n * es;
+  s.ts = std::max(sys->table_len, 1LL) * es;
+  s.cs = (sys->M + sys->nnz) * es;
+  s.as = m * (n + 1) * es;
+  s.qs = m * n * es;
+  s.rs = (n + 1) * (n + 1) * es;
+  s.ks = m * es;
+  auto mk = [&](DevBuf &b, long long per) { b = DevBuf((size_t)W * per * sizeof(double) + 16, st); };
+  mk(s.x, s.xs);
+  mk(s.dx, s.xs);
+  mk(s.table, s.ts);
+  mk(s.contrib, s.cs);
+  mk(s.A, s.as);
+  mk(s.Q, s.qs);
+  mk(s.R, s.rs);
+  mk(s.k, s.ks);
+  s.flags = DevBuf((size_t)W * sizeof(int32_t) + 16, st);
+  s.list = DevBuf((size_t)W * sizeof(int32_t) + 16, st);
+}
+
+// Batched runs: W slots hold W starts at a time.  Every iteration evaluates
+// all busy slots in one pass of the evaluation kernels (blockIdx.y = slot)
+// and solves them with one k_solve_batch launch (one CTA per start); the
+// host then retires converged / failed / exhausted starts and refills their
+// slots from the queue, so the GPU stays full until the queue drains.
+extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
+                               double tol, double *x_out, int32_t *iters, int32_t *status, void *stream) {
+  PN_API_BEGIN
+  PN_REQUIRE(sys && x0 && x_out && iters && status && B >= 0 && max_iters >= 1, PN_E_ARG,
+             "pn_newton_batch: bad arguments");
+  const int m = sys->m, n = sys->n, es = sys->es;
+  PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf cpos_d(sizeof(int32_t) * (m + 1), st);
+  if (consts) constant_positions(sys, cpos_d, st);
+  const char *mode = getenv("PN_BATCH_MODE");
+  if ((mode && strcmp(mode, "serial") == 0) || m > 1024) {
+    newton_batch_serial(sys, B, x0, consts, max_iters, tol, x_out, iters, status, st, cpos_d);
+    return PN_OK;
+  }
+  const size_t ebytes = (size_t)es * sizeof(double);
+  DevIn xin(x0, (size_t)B * n * es, st);
+  DevIn cin(consts, consts ? (size_t)B * m * es : 0, st);
+  DevBuf xa_all((size_t)B * n * ebytes + 16, st), ca_all(consts ? (size_t)B * m * ebytes + 16 : 16, st);
+  if (B) planes_to_aos(es, B * n, xin.d, xa_all.d(), st);
+  if (consts && B) planes_to_aos(es, B * m, cin.d, ca_all.d(), st);
+  const int W = B ? batch_width(sys, B) : 0;
+  BatchSlots s;
+  if (W) batch_alloc(sys, s, W, st);
+  std::vector<int64_t> owner(W, -1);
+  std::vector<int32_t> it((size_t)B, 0), flags(W), list;
+  int64_t next = 0;
+  auto load = [&](int slot) {
+    if (next >= B) {
+      owner[slot] = -1;
+      return;
+    }
+    const int64_t b = next++;
+    owner[slot] = b;
+    PN_CHECK_CUDA(cudaMemcpyAsync(s.x.d() + slot * s.xs, xa_all.d() + b * n * es, n * ebytes,
+                                  cudaMemcpyDeviceToDevice, st));
+    if (consts)
+      PN_CHECK_CUDA(cudaMemcpyAsync(s.k.d() + slot * s.ks, ca_all.d() + b * m * es, m * ebytes,
+                                    cudaMemcpyDeviceToDevice, st));
+  };
+  for (int w = 0; w < W; ++w) load(w);
+  while (true) {
+    list.clear();
+    for (int w = 0; w < W; ++w)
+      if (owner[w] >= 0) list.push_back(w);
+    if (list.empty()) break;
+    const int nb = (int)list.size();
+    PN_CHECK_CUDA(cudaMemcpyAsync(s.list.p, list.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
+    const int32_t *sl = s.list.as<int32_t>();
+    const BView bv{sl, s.xs, s.ts, s.cs, s.as, 0};
+    dispatch_level(sys->nc, sys->cplx, [&]<class E>() {
+      evaldiff_batch_impl<E>(sys, nb, bv, s.x.d(), s.table.d(), s.contrib.d(), nullptr, s.A.d(), n,
+                             cpos_d.as<int32_t>(), consts ? s.k.d() : nullptr, s.ks, st);
+      solve_batch_impl<E>(nb, sl, m, n, s.A.d(), s.as, s.Q.d(), s.qs, s.R.d(), s.rs, s.x.d(), s.xs, s.dx.d(), tol,
+                          s.flags.as<int32_t>(), st);
+    });
+    PN_CHECK_CUDA(cudaMemcpyAsync(flags.data(), s.flags.p, sizeof(int32_t) * W, cudaMemcpyDeviceToHost, st));
+    PN_CHECK_CUDA(cudaStreamSynchronize(st));
+    for (int w : list) {
+      const int64_t b = owner[w];
+      const int f = flags[w];
+      ++it[b];
+      int stat = -1;
+      if (f == 1) stat = 0;
+      else if (f == 2) stat = 2;
+      else if (f == 3) stat = 3;
+      else if (it[b] >= max_iters) stat = 1;
+      if (stat < 0) continue;
+      iters[b] = it[b];
+      status[b] = stat;
+      PN_CHECK_CUDA(cudaMemcpyAsync(xa_all.d() + b * n * es, s.x.d() + w * s.xs, n * ebytes,
+                                    cudaMemcpyDeviceToDevice, st));
+      load(w);
+    }
+  }
+  DevOut xo(x_out, (size_t)B * n * es, st);
+  if (B) aos_to_planes(es, B * n, xa_all.d(), xo.d, st);
+  xo.finish(st);
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));
   PN_API_END
 }
 
-// values f(x_b) of a batch of points (planes (cshape, B, n) -> (cshape, B, m))
+// values f(x_b) of a batch of points (planes (cshape, B, n) -> (cshape, B, m)),
+// evaluated W points at a time through the batched evaluation kernels
 extern "C" int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, double *f, void *stream) {
   PN_API_BEGIN
   PN_REQUIRE(sys && x && f && B >= 0, PN_E_ARG, "pn_evaldiff_batch: bad arguments");
@@ -254,9 +391,21 @@ extern "C" int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, dou
   DevIn xin(x, (size_t)B * n * es, st);
   DevBuf xa((size_t)B * n * ebytes + 16, st), fa((size_t)B * m * ebytes + 16, st);
   if (B) planes_to_aos(es, B * n, xin.d, xa.d(), st);
-  sys->Abuf.ensure((size_t)std::max(m, 1) * (n + 1) * ebytes);
-  for (int64_t b = 0; b < B; ++b)
-    evaldiff_device(sys, xa.d() + (size_t)b * n * es, fa.d() + (size_t)b * m * es, sys->Abuf.d(), m, -1, st);
+  const int W = B ? batch_width(sys, B) : 0;
+  if (W) {
+    const long long ts = std::max(sys->table_len, 1LL) * es, cs = (sys->M + sys->nnz) * es;
+    const long long as = (long long)std::max(m, 1) * (n + 1) * es;
+    DevBuf table((size_t)W * ts * sizeof(double) + 16, st), contrib((size_t)W * cs * sizeof(double) + 16, st);
+    DevBuf A((size_t)W * as * sizeof(double) + 16, st);
+    for (int64_t b0 = 0; b0 < B; b0 += W) {
+      const int nb = (int)std::min<int64_t>(W, B - b0);
+      const BView bv{nullptr, (long long)n * es, ts, cs, as, (long long)m * es};
+      dispatch_level(sys->nc, sys->cplx, [&]<class E>() {
+        evaldiff_batch_impl<E>(sys, nb, bv, xa.d() + b0 * n * es, table.d(), contrib.d(), fa.d() + b0 * m * es,
+                               A.d(), -1, nullptr, nullptr, 0, st);
+      });
+    }
+  }
   DevOut fo(f, (size_t)B * m * es, st);
   if (B) aos_to_planes(es, B * m, fa.d(), fo.d, st);
   fo.finish(st);

@@ -106,3 +106,82 @@ def test_batch_matches_single_runs(gpu, lv):
         assert same(res.x[..., b, :], level.to_planes(tr.x)), b
         assert res.iters[b] == len(tr.entries)
         assert res.status[b] == (0 if tr.converged else 1)
+
+
+def _single_runs(p, Z, t, level, max_iters):
+    from paper_1402_2626_b200.newton import NewtonConfig, homotopy_start_system, run_newton
+    out = []
+    for b in range(Z.shape[-2]):
+        zb = np.ascontiguousarray(Z[..., b, :])
+        single = homotopy_start_system(p, zb, t)
+        out.append(run_newton(single, zb, NewtonConfig(level=level, max_iters=max_iters)))
+    return out
+
+
+def _check_batch_vs_single(lv, n, T, k, B, max_iters, seed, m=None, slots=None):
+    from paper_1402_2626_b200.batch import homotopy_batch, run_newton_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    from paper_1402_2626_b200.generators import random_point, random_sparse_system, random_unit_point
+    level = level_from_name(lv)
+    kw = {} if m is None else {"m": m}
+    p = random_sparse_system(n, T, k, level, seed=seed, maxexp=2, **kw)
+    gen = random_unit_point if level.cplx else random_point
+    Z = np.stack([level.to_planes(gen(n, 1000 + seed + b, level)) for b in range(B)], axis=-2)
+    t = level.from_float(0.99)
+    system, consts = homotopy_batch(p, Z, t)
+    old = os.environ.get("PN_BATCH_SLOTS")
+    if slots is not None:
+        os.environ["PN_BATCH_SLOTS"] = str(slots)
+    try:
+        res = run_newton_batch(PreparedSystem(system), Z, consts, max_iters=max_iters)
+    finally:
+        if slots is not None:
+            if old is None:
+                del os.environ["PN_BATCH_SLOTS"]
+            else:
+                os.environ["PN_BATCH_SLOTS"] = old
+    for b, tr in enumerate(_single_runs(p, Z, t, level, max_iters)):
+        assert same(res.x[..., b, :], level.to_planes(tr.x)), (lv, b)
+        assert res.iters[b] == len(tr.entries), (lv, b)
+        assert res.status[b] == (0 if tr.converged else 1), (lv, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lv", ["cd", "cdd", "cqd", "rdd", "rqd"])
+def test_batch_multi_panel(gpu, lv):
+    """n = 40 spans several left-looking panels (P = 8/16/32) with a ragged last one."""
+    _check_batch_vs_single(lv, 40, 6, 3, 3, 6, seed=11)
+
+
+@pytest.mark.gpu
+def test_batch_slot_refill(gpu):
+    """More starts than slots: retired slots are refilled from the queue."""
+    _check_batch_vs_single("cdd", 24, 5, 3, 7, 8, seed=5, slots=2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lv,n,m", [("cdd", 40, 56), ("cd", 300, 300), ("cdd", 520, 520), ("cqd", 260, 270)])
+def test_batch_row_blocks(gpu, lv, n, m):
+    """Overdetermined systems and every rows-per-thread variant (m <= 256, 512, 1024)."""
+    _check_batch_vs_single(lv, n, 3, 2, 2, 2, seed=3, m=m)
+
+
+@pytest.mark.gpu
+def test_batch_breakdown_status(gpu):
+    """A variable that appears nowhere gives a zero Jacobian column: MGS breakdown
+    (mgs.py:176-181) is reported per start and x keeps its last value."""
+    from paper_1402_2626_b200.batch import homotopy_batch, run_newton_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    from paper_1402_2626_b200.generators import random_sparse_system, random_unit_point
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    level = level_from_name("cdd")
+    p = random_sparse_system(12, 5, 3, level, seed=9, maxexp=1, m=13)
+    # widen to 13 variables: x12 never appears
+    q = PackedSystem(level, 13, p.poly_ptr, p.mon_ptr, p.var_idx, p.exps, p.coeffs)
+    B = 3
+    Z = np.stack([level.to_planes(random_unit_point(13, 50 + b, level)) for b in range(B)], axis=-2)
+    system, consts = homotopy_batch(q, Z, level.from_float(0.99))
+    res = run_newton_batch(PreparedSystem(system), Z, consts, max_iters=5)
+    assert list(res.status) == [2] * B
+    assert list(res.iters) == [1] * B
+    assert same(res.x, Z)
