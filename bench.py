@@ -399,8 +399,13 @@ def run_batched(args):
     t = level.from_float(0.99)
     system, consts = homotopy_batch(packed, Zs, t)
     prep = PreparedSystem(system)
-    # warm-up on one start, then the timed shard
-    run_newton_batch(prep, Zs[..., :1, :], consts[..., :1, :], max_iters=1)
+    lib = _lib.load()
+    import ctypes
+    peak = ctypes.c_double(0)
+    _lib.check(lib.pn_fp64_peak(ctypes.byref(peak), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    # warm-up: one iteration of the whole shard (sizes every slot buffer), then the timed run
+    for _ in range(max(1, args.warmup)):
+        run_newton_batch(prep, Zs, consts, max_iters=1)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -429,6 +434,11 @@ def run_batched(args):
     g0 = time.perf_counter()
     full = gather_batch(res, B)
     gather_s = time.perf_counter() - g0
+    # FP64 roofline of the whole run: every start-iteration is one evaluation
+    # plus one MGS least-squares solve of the (m x n) system
+    w_eval, w_mgs, _ = work_counts(prep.stats(), level.ncomp, level.cplx, system.n_eqs, system.n_vars)
+    achieved = total_iters * (w_eval + w_mgs) / elapsed / 1e12
+    fp64_peak = peak.value / 1e12
     if rank == 0:
         counts = {name: int((full.status == code).sum()) for code, name in
                   [(0, "converged"), (1, "max_iters"), (2, "breakdown"), (3, "singular")]}
@@ -442,7 +452,12 @@ def run_batched(args):
                        "starts": B, "starts_per_gpu": hi - lo, "parallelism": f"start-sharded x{world}",
                        "collective": "one all_gather (status, iterations, x) after the run"},
             "status": counts, "mean_iters": float(full.iters.mean()) if B else 0.0,
-            "gather_s": gather_s, "gpu_launches": launches, "clocks": clk}))
+            "gather_s": gather_s, "gpu_launches": launches, "clocks": clk,
+            "roofline": {"bound": "fp64", "kernel": "k_solve_batch + k_mono_tree + k_segments (whole run)",
+                         "achieved": achieved, "peak": fp64_peak * world, "unit": "T FP64-instr/s",
+                         "frac": achieved / (fp64_peak * world), "traffic": None,
+                         "peak_source": "measured in-run DFMA probe (pn_fp64_peak), per GPU x n_gpus",
+                         "work_fp64_instr_per_start_iteration": w_eval + w_mgs}}))
     dist.destroy_process_group()
 
 

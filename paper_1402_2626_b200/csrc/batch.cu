@@ -24,6 +24,9 @@
 // shuffle level halves the columns a lane carries, so no addition is done
 // twice) followed by a tree over warps; every reduction keeps tree_sum's
 // right-pruned pairwise order.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -153,8 +156,8 @@ template <int NT> __device__ __forceinline__ double block_max(double v, double *
   return r;
 }
 
-template <class E, int B, int P, int NT>
-__global__ void __launch_bounds__(NT, 1)
+template <class E, int B, int P, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
     k_solve_batch(const int32_t *__restrict__ slots, int m, int n, double *__restrict__ Aall, long long As,
                   double *__restrict__ Qall, long long Qs, double *__restrict__ Rall, long long Rs,
                   double *__restrict__ xall, long long xs, double *__restrict__ dxall, double eps, double tol,
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-template <class E, int B, int P>
+template <class E, int B, int P, int MINB>
 static void launch_solve(int nb, const int32_t *slots, int m, int n, double *A, long long As, double *Q,
                          long long Qs, double *R, long long Rs, double *x, long long xs, double *dx, double eps,
                          double tol, int32_t *flags, cudaStream_t st) {
@@ -367,7 +370,7 @@ static void launch_solve(int nb, const int32_t *slots, int m, int n, double *A, 
   const size_t bsub = (size_t)n * (2 * es + Traits<E>::nc) * sizeof(double);
   const size_t smem = std::max(pan, bsub) + (size_t)(NT / 32 + 1) * P * es * sizeof(double);
   PN_REQUIRE(smem <= 227 * 1024, PN_E_ARG, "batched solve: n=%d needs %zu B of shared memory", n, smem);
-  auto kern = k_solve_batch<E, B, P, NT>;
+  auto kern = k_solve_batch<E, B, P, NT, MINB>;
   PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<nb, NT, smem, st>>>(slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags);
   PN_CHECK_LAUNCH();
@@ -383,9 +386,19 @@ void solve_batch_impl(int nb, const int32_t *slots, int m, int n, double *A, lon
   PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
   PN_REQUIRE(m <= 1024, PN_E_ARG, "batched solve supports m <= 1024 rows (got %d)", m);
   if (nb <= 0) return;
-  if (m <= 256) launch_solve<E, 1, PM>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
-  else if (m <= 512) launch_solve<E, 2, PM / 2>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
-  else launch_solve<E, 4, PM / 4>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+  // default "narrow": half the panel width and two CTAs per SM (more warps
+  // to hide FP64 latency, twice the Q traffic): 3524 vs 3120 start-iterations/s
+  // on C5 (profiles/r01); "wide" = full panel, one CTA per SM
+  const char *v = getenv("PN_SOLVE_VARIANT");
+  const bool narrow = !(v && strcmp(v, "wide") == 0);
+  if (m <= 256) {
+    if (narrow) launch_solve<E, 1, PM / 2, 2>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+    else launch_solve<E, 1, PM, 1>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+  } else if (m <= 512) {
+    launch_solve<E, 2, PM / 2, 1>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+  } else {
+    launch_solve<E, 4, PM / 4, 1>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+  }
 }
 
 #ifdef PN_NC

@@ -116,6 +116,38 @@ __device__ __forceinline__ E block_tree_reduce(E v, int nparts, E *sm) {
   return v;
 }
 
+// The same tree with a single barrier: every warp writes its partial into
+// half `parity` of sm (2*NT/32 elements), and after one __syncthreads every
+// warp reduces the NT/32 partials itself with the same absorb rule.  The
+// redundant cross-warp levels cost log2(NT/32) additions per warp but remove
+// two barriers from the critical path; alternating `parity` between
+// consecutive calls makes the reuse of sm race-free without a trailing
+// barrier.
+template <class E, int NT>
+__device__ __forceinline__ E block_tree_reduce_1bar(E v, int nparts, E *sm, int parity) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    E o = eshfl_down(v, s);
+    if ((lane & (2 * s - 1)) == 0 && t + s < nparts) v = eadd(v, o);
+  }
+  constexpr int NW = NT / 32;
+  if constexpr (NW > 1) {
+    E *h = sm + (parity & 1) * NW;
+    if (lane == 0) h[w] = v;
+    __syncthreads();
+    const int nw = (nparts + 31) / 32;
+    E x = h[lane < NW ? lane : 0];
+#pragma unroll
+    for (int s = 1; s < NW; s <<= 1) {
+      E o = eshfl_down(x, s);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < nw) x = eadd(x, o);
+    }
+    v = x;
+  }
+  return eshfl_idx(v, 0);
+}
+
 // sequential pairwise tree over a register array of B elements where only
 // the first `valid` are present (aligned block; right-pruned)
 template <class E, int B>

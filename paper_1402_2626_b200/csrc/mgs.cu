@@ -724,12 +724,21 @@ void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStr
 // rows above are updated by the rest of the grid, one thread per row.  Every
 // row still receives its subtractions in descending column order, so x is
 // bit-identical to the reference's sequential solve (mgs.py:229-247).
+// The solver's operands (the diagonal block, the block above it and the
+// hoisted reciprocals) are staged in shared memory with all loads in flight
+// at once, so the sequential chain never waits on L2.
 template <class E, int NT>
 __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict__ R, int n, double *__restrict__ x,
                                                         RDiv<Traits<E>::nc> *__restrict__ prep,
                                                         double *__restrict__ y, int *sing, MgsStatus *status) {
   namespace cg = cooperative_groups;
+  using RD = RDiv<Traits<E>::nc>;
   constexpr int es = Traits<E>::es;
+  extern __shared__ __align__(16) double bs_smem[];
+  E *sD = reinterpret_cast<E *>(bs_smem);  // 32 x 32 diagonal block, column-major
+  E *sU = sD + 32 * 32;                     // 32 x 32 block above it (rows lo-32..lo-1)
+  E *sX = sU + 32 * 32;                     // x of the current block
+  RD *sP = reinterpret_cast<RD *>(sX + 32);
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;  // the factorisation failed (uniform for all CTAs)
   const long long ld = n + 1;
@@ -762,30 +771,44 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict
   for (int b = nb - 1; b >= 0; --b) {
     const int lo = b * 32, hi = min(n, lo + 32);
     if (solver) {
+      // stage the diagonal block (rows lo..j of column j) and the reciprocals
+      for (int jj = 0; jj < hi - lo; ++jj)
+        if (lane <= jj) sD[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo + lane) * es);
+      if (lo + lane < hi) sP[lane] = prep[lo + lane];
+      __syncwarp();
       E xl = ezero<E>();
       for (int j = hi - 1; j >= lo; --j) {
         const int jl = j - lo;
-        if (lane == jl) xl = ediv_with(yr, eload<E>(R + ((long long)j * ld + j) * es), prep[j]);
+        if (lane == jl) xl = ediv_with(yr, sD[jl * 32 + jl], sP[jl]);
         const E xj = eshfl_idx(xl, jl);
-        if (lane < jl) yr = esub(yr, emul(eload<E>(R + ((long long)j * ld + lo + lane) * es), xj));
+        if (lane < jl) yr = esub(yr, emul(sD[jl * 32 + lane], xj));
       }
-      if (lo + lane < hi) estore(x + (long long)(lo + lane) * es, xl);
+      if (lo + lane < hi) {
+        estore(x + (long long)(lo + lane) * es, xl);
+        sX[lane] = xl;
+      }
+      __syncwarp();
     }
     grid.sync();
     if (b == 0) break;
     // rows of block b-1 (solver warp) and all rows above it (rest of the grid)
     if (solver) {
       const int r = lo - 32 + lane;
+      for (int jj = 0; jj < hi - lo; ++jj) sU[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + r) * es);
       yr = eload<E>(y + (long long)r * es);
-      for (int j = hi - 1; j >= lo; --j)
-        yr = esub(yr, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+      __syncwarp();
+      for (int j = hi - 1; j >= lo; --j) yr = esub(yr, emul(sU[(j - lo) * 32 + lane], sX[j - lo]));
     } else {
       const int worker = blockIdx.x == 0 ? threadIdx.x - 32 : gtid - 32;
       const int workers = gsize - 32;
       for (int r = worker; r < lo - 32; r += workers) {
         E v = eload<E>(y + (long long)r * es);
-        for (int j = hi - 1; j >= lo; --j)
-          v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+        E rn = eload<E>(R + ((long long)(hi - 1) * ld + r) * es);
+        for (int j = hi - 1; j >= lo; --j) {
+          const E rc = rn;
+          if (j > lo) rn = eload<E>(R + ((long long)(j - 1) * ld + r) * es);
+          v = esub(v, emul(rc, eload<E>(x + (long long)j * es)));
+        }
         estore(y + (long long)r * es, v);
       }
     }
@@ -808,7 +831,10 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
     double *yp = yw.d();
     MgsStatus *status = w.status.as<MgsStatus>();
     void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
-    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_blocked<E, NT>, grid, NT, args, 0, st));
+    const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<Traits<E>::nc>);
+    PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_blocked<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_blocked<E, NT>, grid, NT, args, smem, st));
     count_launch(1);
     return;
   }

@@ -32,7 +32,25 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// keep freed stream-ordered memory in the device pool instead of returning
+// it at every synchronisation: batched runs allocate tens of GB of slots per
+// call, and re-mapping them each time costs more than a Newton iteration
+static void keep_pool_memory() {
+  static const bool done = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    return true;
+  }();
+  (void)done;
+}
+
 DevBuf::DevBuf(size_t nbytes, cudaStream_t st) : bytes(nbytes), s(st) {
+  keep_pool_memory();
   if (nbytes) PN_CHECK_CUDA(cudaMallocAsync(&p, nbytes, st));
 }
 DevBuf::~DevBuf() {
