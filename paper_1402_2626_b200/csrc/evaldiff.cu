@@ -23,6 +23,9 @@
 //   K2 k_segments    : one thread per output entry; a binary-counter fold of
 //                      the entry's contributions reproduces tree_sum's
 //                      right-pruned pairwise order exactly.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -117,34 +120,24 @@ __device__ __forceinline__ E monomial_scale(const E &co, int lo, int k, const in
 template <int V> struct Log2 { static constexpr int value = 1 + Log2<V / 2>::value; };
 template <> struct Log2<1> { static constexpr int value = 0; };
 
-template <class E, int BASE, int G, int NT>
-__global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ list, long long count,
-                                                  const int32_t *__restrict__ mon_ptr,
-                                                  const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
-                                                  const int32_t *__restrict__ dst, const double *__restrict__ coeff,
-                                                  const double *__restrict__ x, const double *__restrict__ table,
-                                                  const int32_t *__restrict__ toff, double *__restrict__ contrib,
-                                                  BView bv) {
+// One monomial with 2 <= k <= 32 on a group of G lanes (lane r of the group
+// passes r).  mv / me: the monomial's variable indices and exponents (global
+// or shared memory).
+// Results go through two sinks: value(v) on lane 0 of the group and
+// deriv(t, v) for every support position t of the monomial.  Inactive
+// groups (active == false) run the shuffles but emit nothing.
+template <class E, int BASE, int G, class VSink, class DSink>
+__device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const int32_t *mv, const int32_t *me,
+                                               const E &co, const double *__restrict__ x,
+                                               const double *__restrict__ table, const int32_t *__restrict__ toff,
+                                               VSink &&value_sink, DSink &&deriv_sink) {
   constexpr int es = Traits<E>::es;
-  {
-    const long long b = bslot(bv);
-    x += b * bv.x;
-    table += b * bv.t;
-    contrib += b * bv.c;
-  }
   constexpr int SL = BASE / G;            // slots per lane
   constexpr int NLOC = Log2<SL>::value;   // lane-local levels above the slots
   constexpr int NX = Log2<G>::value;      // butterfly levels
   constexpr int NLV = SL > 1 ? SL - 1 : 1;
   static_assert(BASE >= G && G >= 2 && G <= 32, "bad tree config");
-
-  const long long grp = (blockIdx.x * (long long)NT + threadIdx.x) / G;
-  const int r = threadIdx.x % G;
-  const bool active = grp < count;
-  const int c = list[active ? grp : count - 1];
-  const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
   const int ell = k - BASE;
-  const int32_t *__restrict__ mv = var + lo;
 
   auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
   // slot t of level 0: v[t] * v[BASE+t] for t < ell, else v[t] (evaldiff.py:63-65)
@@ -183,9 +176,8 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
   const E root = X[NX];
 
   // ---- value (evaldiff.py:166-172) ---------------------------------------
-  const E co = eload<E>(coeff + (long long)c * es);
-  const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
-  if (active && r == 0) estore(contrib + (long long)c * es, emul(scale, root));
+  const E scale = monomial_scale<E>(co, 0, k, mv, me, table, toff);
+  if (active && r == 0) value_sink(emul(scale, root));
 
   // ---- downward sweep of complements (evaldiff.py:89-98) -----------------
   // complement of this lane's node at the current level
@@ -232,17 +224,220 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
       const int t2 = BASE + t;
       const E g1 = emul(cl[u], leaf(t2));
       const E g2 = emul(cl[u], leaf(t));
-      const int d1 = exps[lo + t], d2 = exps[lo + t2];
+      const int d1 = me[t], d2 = me[t2];
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
       const E s2 = d2 == 1 ? scale : emul_int(scale, d2);
-      estore(contrib + (long long)dst[lo + t] * es, emul(s1, g1));
-      estore(contrib + (long long)dst[lo + t2] * es, emul(s2, g2));
+      deriv_sink(t, emul(s1, g1));
+      deriv_sink(t2, emul(s2, g2));
     } else {
-      const int d1 = exps[lo + t];
+      const int d1 = me[t];
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
-      estore(contrib + (long long)dst[lo + t] * es, emul(s1, cl[u]));
+      deriv_sink(t, emul(s1, cl[u]));
     }
   }
+}
+
+template <class E, int BASE, int G, int NT>
+__global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ list, long long count,
+                                                  const int32_t *__restrict__ mon_ptr,
+                                                  const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                                                  const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                                                  const double *__restrict__ x, const double *__restrict__ table,
+                                                  const int32_t *__restrict__ toff, double *__restrict__ contrib,
+                                                  BView bv) {
+  constexpr int es = Traits<E>::es;
+  {
+    const long long b = bslot(bv);
+    x += b * bv.x;
+    table += b * bv.t;
+    contrib += b * bv.c;
+  }
+  const long long grp = (blockIdx.x * (long long)NT + threadIdx.x) / G;
+  const int r = threadIdx.x % G;
+  const bool active = grp < count;
+  const int c = list[active ? grp : count - 1];
+  const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
+  const E co = eload<E>(coeff + (long long)c * es);
+  mono_tree_eval<E, BASE, G>(
+      r, active, k, var + lo, exps + lo, co, x, table, toff,
+      [&](const E &v) { estore(contrib + (long long)c * es, v); },
+      [&](int t, const E &v) { estore(contrib + (long long)dst[lo + t] * es, v); });
+}
+
+// ---------------------------------------------------------------------------
+// Fused evaluation for batches (config C5): one CTA per (polynomial, slot)
+// evaluates the polynomial's monomials chunk by chunk (CH = NT/G monomials
+// in canonical order, supports staged in shared memory) and folds every
+// contribution straight into per-variable binary-counter stacks in shared
+// memory -- the streaming form of tree_sum's pairwise order --
+// so f and the Jacobian row never round-trip through a contribution buffer.
+// Within a chunk the derivative contributions land in (var, monomial) order
+// (host-computed ldst), each variable's run is pushed by one thread, and the
+// chunk's values are reduced by a warp tree and pushed at chunk granularity
+// (full chunks are aligned blocks of the counter).  Systems whose monomials
+// all have k in {0, K} (2 <= K <= 32) and whose stacks fit shared memory use
+// this path (pn_system::Fused); everything else uses K1 + K2.
+
+template <class E> struct TreeG;  // lanes per monomial, by precision
+template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
+template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
+
+// binary-counter stack: level l of the stack lives at st[l * stride]
+template <class E>
+__device__ __forceinline__ void stack_push(E *st, int stride, int cnt, E v) {
+  int l = 0;
+  while ((cnt >> l) & 1) {
+    v = eadd(st[l * stride], v);  // the older (lower-index) block stays on the left
+    ++l;
+  }
+  st[l * stride] = v;
+}
+
+template <class E>
+__device__ __forceinline__ E stack_fold(const E *st, int stride, int cnt) {
+  int l = __ffs(cnt) - 1;
+  E acc = st[l * stride];
+  for (++l; l < 31; ++l)
+    if ((cnt >> l) & 1) acc = eadd(st[l * stride], acc);
+  return acc;
+}
+
+template <class E, int BASE, int G, int NT>
+__global__ void __launch_bounds__(NT) k_eval_fused(int m, int n, int D, int K, const int64_t *__restrict__ poly_ptr,
+                                                   const int32_t *__restrict__ mon_ptr,
+                                                   const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                                                   const int16_t *__restrict__ ldst, const double *__restrict__ coeff,
+                                                   const int32_t *__restrict__ seg_var,
+                                                   const int32_t *__restrict__ seg_sl,
+                                                   const int32_t *__restrict__ chunk_seg,
+                                                   const int32_t *__restrict__ poly_chunk,
+                                                   const double *__restrict__ x, const double *__restrict__ table,
+                                                   const int32_t *__restrict__ toff, const double *__restrict__ consts,
+                                                   long long cstride, double *__restrict__ f, double *__restrict__ A,
+                                                   int negf_col, BView bv) {
+  constexpr int es = Traits<E>::es;
+  constexpr int CH = NT / G;
+  constexpr int VL = 24;  // value-stack levels (chunk granularity)
+  extern __shared__ __align__(16) double fz_smem[];
+  E *stk = reinterpret_cast<E *>(fz_smem);            // D levels x n variables (level-major)
+  E *buf = stk + (size_t)n * D;                       // CH values + CH*K derivatives
+  E *vstk = buf + CH * (1 + K);                       // VL
+  int *cnt = reinterpret_cast<int *>(vstk + VL);      // n
+  // supports of the chunk, monomial u at u*KP (KP = K+1: odd stride, no bank conflicts)
+  const int KP = K + 1;
+  int *svar = cnt + n;                                // CH*KP + 32 (zero pad)
+  int *sexp = svar + CH * KP + 32;
+  int *sdst = sexp + CH * KP + 32;
+  const int PAD = CH * KP;
+
+  const int i = blockIdx.x;
+  const long long b = bslot(bv);
+  x += b * bv.x;
+  table += b * bv.t;
+  A += b * bv.a;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int j = tid; j < n; j += NT) cnt[j] = 0;
+  if (tid < 32) {
+    svar[PAD + tid] = 0;  // inactive groups read this pad
+    sexp[PAD + tid] = 1;
+  }
+  const long long p0 = poly_ptr[i];
+  const int T = (int)(poly_ptr[i + 1] - p0);
+  const int gc0 = poly_chunk[i], nch = poly_chunk[i + 1] - gc0;
+  E value = ezero<E>();  // f_i; zero_like for an empty polynomial (evaldiff.py:261)
+  for (int c = 0; c < nch; ++c) {
+    const long long cm0 = p0 + (long long)c * CH;
+    const int U = min(CH, T - c * CH);
+    const int e0 = mon_ptr[cm0], ne = mon_ptr[cm0 + U] - e0;
+    __syncthreads();  // the previous chunk's pushes are done with buf / supports
+    int lead = 0;  // constant monomials sort first (k = 0, no support entries)
+    while (lead < U && mon_ptr[cm0 + lead + 1] == e0) ++lead;
+    for (int e = tid; e < ne; e += NT) {
+      const int pos = (lead + e / K) * KP + e % K;
+      svar[pos] = var[e0 + e];
+      sexp[pos] = exps[e0 + e];
+      sdst[pos] = CH + ldst[e0 + e];
+    }
+    __syncthreads();
+    // ---- monomials: group g of G lanes takes monomial u = g of the chunk
+    const int u = tid / G, r = tid % G;
+    const long long cm = cm0 + (u < U ? u : 0);
+    const int lo = mon_ptr[cm], k = mon_ptr[cm + 1] - lo;
+    const bool tree = u < U && k > 0;
+    if (u < U && k == 0 && r == 0) {  // constant term (evaldiff.py:152-153); per-start shift if given
+      buf[u] = consts ? eload<E>(consts + b * cstride + (long long)i * es) : eload<E>(coeff + cm * es);
+    }
+    const int off = tree ? u * KP : PAD;
+    const E co = tree ? eload<E>(coeff + cm * es) : ezero<E>();
+    mono_tree_eval<E, BASE, G>(
+        r, tree, tree ? k : BASE, svar + off, sexp + off, co, x, table, toff, [&](const E &v) { buf[u] = v; },
+        [&](int t, const E &v) { buf[sdst[off + t]] = v; });
+    __syncthreads();
+    // ---- per-variable pushes, one thread per variable run of the chunk
+    const int s0 = chunk_seg[gc0 + c], s1 = chunk_seg[gc0 + c + 1];
+    for (int s = s0 + tid; s < s1; s += NT) {
+      const int j = seg_var[s], sl = seg_sl[s];
+      const int st = sl & 0xffff, len = sl >> 16;
+      int cj = cnt[j];
+      for (int q = 0; q < len; ++q, ++cj) stack_push(stk + j, n, cj, buf[CH + st + q]);
+      cnt[j] = cj;
+    }
+    // ---- values: warp tree of the chunk (right-pruned), pushed per chunk
+    if (tid < 32) {
+      E v = lane < U ? buf[lane] : ezero<E>();
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const E o = eshfl_down(v, s);
+        if ((lane & (2 * s - 1)) == 0 && lane + s < U) v = eadd(v, o);
+      }
+      if (lane == 0) {
+        if (c + 1 < nch) {
+          stack_push(vstk, 1, c, v);
+        } else {  // last chunk: fold the chunk-level counter (c full chunks)
+          E acc = v;
+          for (int l = 0; l < VL; ++l)
+            if ((c >> l) & 1) acc = eadd(vstk[l], acc);
+          value = acc;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- Jacobian row i (column-major, ld = m) and the b column
+  for (int j = tid; j < n; j += NT) {
+    const int L = cnt[j];
+    estore(A + ((long long)j * m + i) * es, L ? stack_fold(stk + j, n, L) : ezero<E>());
+  }
+  if (tid == 0) {
+    if (f) estore(f + b * bv.f + (long long)i * es, value);
+    if (negf_col >= 0) estore(A + ((long long)negf_col * m + i) * es, eneg(value));
+  }
+}
+
+template <class E>
+static size_t fused_smem(const pn_system *sys) {
+  constexpr int es = Traits<E>::es;
+  const int CH = 32, K = sys->fused.K;
+  return (size_t)es * 8 * ((size_t)sys->n * sys->fused.D + CH * (1 + K) + 24) +
+         4 * ((size_t)sys->n + 3 * (CH * (K + 1) + 32));
+}
+
+template <class E, int BASE>
+static void launch_fused(pn_system *sys, const double *x, const double *table, double *f, double *A, int negf_col,
+                         int nb, const BView &bv, const double *consts, long long cstride, cudaStream_t st) {
+  constexpr int G = TreeG<E>::value < BASE ? TreeG<E>::value : BASE;
+  constexpr int NT = 32 * G;
+  static_assert(NT / G == 32, "fused chunks are 32 monomials");
+  const size_t smem = fused_smem<E>(sys);
+  auto kern = k_eval_fused<E, BASE, G, NT>;
+  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const auto &F = sys->fused;
+  kern<<<dim3(sys->m, nb), NT, smem, st>>>(sys->m, sys->n, F.D, F.K, sys->d_seg_ptr, sys->d_mon_ptr, sys->d_var,
+                                          sys->d_exp, F.d_ldst, sys->d_coeff, F.d_seg_var, F.d_seg_sl,
+                                          F.d_chunk_seg, F.d_poly_chunk, x, table, sys->d_toff, consts, cstride, f,
+                                          A, negf_col, bv);
+  PN_CHECK_LAUNCH();
+  count_launch(1);
 }
 
 // ---------------------------------------------------------------------------
@@ -380,9 +575,6 @@ __global__ void __launch_bounds__(128) k_segments(long long nseg_total, int m, c
 
 // ---------------------------------------------------------------------------
 
-template <class E> struct TreeG;  // lanes per monomial, by precision
-template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
-template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
 
 template <class E, int BASE>
 static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double *x, const double *table,
@@ -419,6 +611,16 @@ __global__ void k_zero_jac(long long count, double *__restrict__ A, BView bv) {
     a[i] = make_double2(0.0, 0.0);
 }
 
+// the fused path serves systems it was planned for (PN_EVAL_FUSED=1 at system
+// creation); PN_EVAL_FUSED=0 at call time turns it off again
+template <class E>
+static bool use_fused(const pn_system *sys, int nb, const BView &bv) {
+  if (!sys->fused.ok) return false;
+  const char *v = getenv("PN_EVAL_FUSED");
+  if (v && strcmp(v, "0") == 0) return false;
+  return fused_smem<E>(sys) <= 200 * 1024;
+}
+
 // the evaluation pipeline for nb slots (nb = 1, zero strides: one system)
 template <class E>
 static void evaldiff_run(pn_system *sys, const double *x, double *table, double *contrib, double *f, double *A,
@@ -430,6 +632,16 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
     k_power_table<E><<<dim3((sys->n + 127) / 128, nb), 128, 0, st>>>(sys->n, x, sys->d_toff, sys->d_tdeg, table, bv);
     PN_CHECK_LAUNCH();
     count_launch(1);
+  }
+  if (use_fused<E>(sys, nb, bv)) {
+    switch (sys->fused.base) {
+      case 2: launch_fused<E, 2>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 4: launch_fused<E, 4>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 8: launch_fused<E, 8>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 16: launch_fused<E, 16>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      default: launch_fused<E, 32>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+    }
+    return;
   }
   for (const auto &b : sys->buckets) {
     if (b.count == 0) continue;

@@ -164,6 +164,18 @@ struct pn_system {
   };
   std::vector<Bucket> buckets;
 
+  // plan of the fused evaluation (k_eval_fused): every monomial has k in
+  // {0, K}; chunks of 32 canonical monomials per polynomial; per support
+  // entry its slot in the chunk's (var, monomial)-sorted contribution list;
+  // per chunk the variable runs (var, start | len << 16)
+  struct Fused {
+    bool ok = false;
+    int K = 0, base = 0, D = 0;
+    long long nchunks = 0, nsegs = 0;
+    int16_t *d_ldst = nullptr;
+    int32_t *d_seg_var = nullptr, *d_seg_sl = nullptr, *d_chunk_seg = nullptr, *d_poly_chunk = nullptr;
+  } fused;
+
   // scratch reused across evaluations
   pn::DevArena contrib;  // (M + nnz) * es
   pn::DevArena table;    // table_len * es

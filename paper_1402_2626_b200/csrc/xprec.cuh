@@ -30,6 +30,10 @@ PN_DI double dsub(double a, double b) { return __dsub_rn(a, b); }
 PN_DI double dmul(double a, double b) { return __dmul_rn(a, b); }
 PN_DI double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 PN_DI double dsqrt(double a) { return __dsqrt_rn(a); }
+// sign flip and "!= 0.0" on the integer pipes: exact, and they keep the FP64
+// pipe (the bottleneck of every dd/qd kernel) for the arithmetic itself
+PN_DI double dneg(double x) { return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x)); }
+PN_DI bool dnz(double x) { return ((__double2hiint(x) & 0x7fffffff) | __double2loint(x)) != 0; }
 
 // ---------------------------------------------------------------------------
 // L0 error-free transforms (_eft.py:22-65)
@@ -77,7 +81,7 @@ template <int NC> struct F { double c[NC]; };
 
 template <int NC> PN_DI F<NC> fzero() { F<NC> r; _Pragma("unroll") for (int i = 0; i < NC; ++i) r.c[i] = 0.0; return r; }
 template <int NC> PN_DI F<NC> fconst(double v) { F<NC> r = fzero<NC>(); r.c[0] = v; return r; }
-template <int NC> PN_DI F<NC> fneg(const F<NC> &a) { F<NC> r; _Pragma("unroll") for (int i = 0; i < NC; ++i) r.c[i] = -a.c[i]; return r; }
+template <int NC> PN_DI F<NC> fneg(const F<NC> &a) { F<NC> r; _Pragma("unroll") for (int i = 0; i < NC; ++i) r.c[i] = dneg(a.c[i]); return r; }
 
 // ---- double (NC = 1): plain IEEE ops ------------------------------------
 PN_DI F<1> fadd(const F<1> &a, const F<1> &b) { F<1> r; r.c[0] = dadd(a.c[0], b.c[0]); return r; }
@@ -123,7 +127,7 @@ PN_DI F<4> renorm5(double c0, double c1, double c2, double c3, double c4) {
     quick_two_sum(cur, t1, s1, e1);
     quick_two_sum(e1, t2, s2, e2);
     quick_two_sum(e2, t3, s3, e3);
-    if (e1 != 0.0 && e2 != 0.0 && e3 != 0.0) {
+    if (dnz(e1) && dnz(e2) && dnz(e3)) {
       r.c[0] = s1; r.c[1] = s2; r.c[2] = s3; r.c[3] = dadd(e3, t4);
       return r;
     }
@@ -134,7 +138,7 @@ PN_DI F<4> renorm5(double c0, double c1, double c2, double c3, double c4) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     quick_two_sum(cur, tv[i], s, e);
-    const bool adv = (e != 0.0) && (k < 3);
+    const bool adv = dnz(e) && (k < 3);
     o0 = (adv && k == 0) ? s : o0;
     o1 = (adv && k == 1) ? s : o1;
     o2 = (adv && k == 2) ? s : o2;
@@ -342,7 +346,7 @@ template <int NC> PN_DI C<NC> emul(const C<NC> &a, const C<NC> &b) { return cmul
 template <int NC> PN_DI C<NC> econj(const C<NC> &a) { return cconj(a); }
 
 template <class E> PN_DI E ezero() { E r; double *p = reinterpret_cast<double *>(&r); _Pragma("unroll") for (int i = 0; i < Traits<E>::es; ++i) p[i] = 0.0; return r; }
-template <class E> PN_DI E eneg(const E &a) { E r; const double *s = reinterpret_cast<const double *>(&a); double *p = reinterpret_cast<double *>(&r); _Pragma("unroll") for (int i = 0; i < Traits<E>::es; ++i) p[i] = -s[i]; return r; }
+template <class E> PN_DI E eneg(const E &a) { E r; const double *s = reinterpret_cast<const double *>(&a); double *p = reinterpret_cast<double *>(&r); _Pragma("unroll") for (int i = 0; i < Traits<E>::es; ++i) p[i] = dneg(s[i]); return r; }
 // one_like (xprec.py:376-383)
 template <class E> PN_DI E eone() { E r = ezero<E>(); reinterpret_cast<double *>(&r)[0] = 1.0; return r; }
 
