@@ -553,7 +553,23 @@ __global__ void __launch_bounds__(128) k_segments(long long nseg_total, int m, c
     if (L == 0) {
       acc = ezero<E>();  // zero_like(point[0]) for an empty polynomial (evaldiff.py:261)
     } else {
-      for (long long p = 0; p < L; ++p) {
+      // aligned blocks of 8: eight independent loads in flight, their
+      // pairwise tree, pushed at level 3 -- the same as eight level-0 pushes
+      long long p = 0;
+      for (; p + 8 <= L; p += 8) {
+        E v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = eload<E>(contrib + (a + p + q) * es);
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) v[q] = eadd(v[q], v[q + 1]);
+        v[0] = eadd(v[0], v[2]);
+        v[4] = eadd(v[4], v[6]);
+        E carry = eadd(v[0], v[4]);
+        int lvl = 3;
+        for (long long q = p >> 3; q & 1; q >>= 1, ++lvl) carry = eadd(stk[lvl], carry);
+        stk[lvl] = carry;
+      }
+      for (; p < L; ++p) {
         E carry = eload<E>(contrib + (a + p) * es);
         int lvl = 0;
         for (long long q = p; q & 1; q >>= 1, ++lvl) carry = eadd(stk[lvl], carry);
