@@ -576,6 +576,143 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_mgs_warp: the latency-bound levels (d, dd) at m <= 32*R.  One warp per
+// column (one-warp CTAs, cooperative launch so every column owner is
+// resident).  Lane l owns the aligned row block [l*R, l*R+R) of its column,
+// kept in shared memory (interleaved: row l*R+i at i*32+l, bank-conflict
+// free), so a sweep is R products per lane, a pairwise tree over the block,
+// and a warp shuffle tree over the lanes (tree_sum's order) --
+// no CTA barriers anywhere on the critical path.  The owner of column k+1
+// sees q_k through an acquire poll, applies sweep k, normalises and
+// publishes q_{k+1}; every other column catches up on its own.  The
+// operation sequence per column is the reference's, so results are
+// bit-identical to the other schedules.
+// pairwise tree (binary counter) over a lane's R-row block, row i supplied
+// by f(i) for i < valid: full blocks (the common case) resolve every level
+// at compile time and stay in registers
+constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
+template <class E, int R, class Fn>
+__device__ __forceinline__ E block_pairwise(int valid, Fn &&f) {
+  constexpr int L = ilog2(R);
+  if (valid == R) {
+    E st[L + 1];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      E v = f(i);
+#pragma unroll
+      for (int l = 0; l <= L; ++l) {
+        if (!((i >> l) & 1)) {
+          st[l] = v;
+          break;
+        }
+        v = eadd(st[l], v);
+      }
+    }
+    return st[L];
+  }
+  Pairwise<E, L + 1> pw;
+  for (int i = 0; i < valid; ++i) pw.push(f(i));
+  return valid > 0 ? pw.fold() : ezero<E>();
+}
+
+template <class E, int R>
+__global__ void __launch_bounds__(32) k_mgs_warp(double *__restrict__ A, int m, int n, double eps,
+                                                 double *__restrict__ Q, double *__restrict__ Rm,
+                                                 MgsStatus *status, int *ready) {
+  using Rl = typename Traits<E>::R;
+  constexpr int es = Traits<E>::es;
+  extern __shared__ __align__(16) double wcol[];  // es planes x (R*32)
+  const int j = blockIdx.x;
+  if (j > n) return;
+  const int lane = threadIdx.x;
+  const int row0 = lane * R;
+  const int nparts = (m + R - 1) / R;
+  const int valid = m - row0 <= 0 ? 0 : (m - row0 >= R ? R : m - row0);
+  auto cget = [&](int i) -> E {
+    E v;
+    double *d = reinterpret_cast<double *>(&v);
+#pragma unroll
+    for (int c = 0; c < es; ++c) d[c] = wcol[c * (R * 32) + i * 32 + lane];
+    return v;
+  };
+  auto cput = [&](int i, const E &v) {
+    const double *d = reinterpret_cast<const double *>(&v);
+#pragma unroll
+    for (int c = 0; c < es; ++c) wcol[c * (R * 32) + i * 32 + lane] = d[c];
+  };
+  // warp tree over the lanes' block partials (absorb rule, right-pruned)
+  auto warp_tree = [&](auto v) {
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const auto o = eshfl_down(v, s);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < nparts) v = eadd(v, o);
+    }
+    return eshfl_idx(v, 0);
+  };
+  auto norm = [&]() -> Rl {
+    return fsqrt(warp_tree(block_pairwise<Rl, R>(valid, [&](int i) { return eabs2(cget(i)); })));
+  };
+  const double *col = A + (long long)j * m * es;
+#pragma unroll
+  for (int i = 0; i < R; ++i) cput(i, row0 + i < m ? eload<E>(col + (long long)(row0 + i) * es) : ezero<E>());
+  // original norm (mgs.py:171-172): only this column's owner needs it
+  const double orig = norm().c[0];
+  const long long ldR = n + 1;
+  for (int k = 0; k < j; ++k) {
+    // wait for pivot k: lane 0 polls, then every lane acquires once
+    if (lane == 0) {
+      long long t0 = clock64();
+      while (ld_acquire(ready + k) == 0) {
+        if (ld_acquire(&status->code) != 0) break;
+        __nanosleep(100);
+        if (clock64() - t0 > (1ll << 36)) {
+          status->k = k;
+          atomicExch(&status->code, PN_E_CUDA);
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (ld_acquire(ready + k) == 0 || ld_acquire(&status->code) != 0) return;
+    const double *qk = Q + (long long)k * m * es;
+    E qv[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) qv[i] = row0 + i < m ? eload_cg<E>(qk + (long long)(row0 + i) * es) : ezero<E>();
+    const E rk = warp_tree(block_pairwise<E, R>(valid, [&](int i) { return emul(econj(qv[i]), cget(i)); }));
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (row0 + i < m) cput(i, esub(cget(i), emul(qv[i], rk)));
+    if (lane == 0) estore(Rm + ((long long)j * ldR + k) * es, rk);
+  }
+  // pivot j (mgs.py:176-193); j == n is the residual norm z
+  const Rl rkk = norm();
+  if (j < n) {
+    const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), orig);
+    if (rkk.c[0] <= thr) {
+      if (lane == 0) {
+        status->k = j;
+        status->rkk = rkk.c[0];
+        status->thr = thr;
+        __threadfence();
+        atomicExch(&status->code, PN_E_BREAKDOWN);
+      }
+      return;
+    }
+  }
+  if (lane == 0) estore(Rm + ((long long)j * ldR + j) * es, eembed(rkk, (E *)nullptr));
+  if (j < n) {
+    const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+    double *qc = Q + (long long)j * m * es;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (row0 + i < m) estore(qc + (long long)(row0 + i) * es, ediv_prepared(cget(i), p));
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(ready + j, 1);
+  }
+}
+
 // back substitution R x = y, y = R[:n, n] (mgs.py:229-247): descending j,
 // x_j = y_j / r_jj (full complex division), y[:j] -= R[:j, j] x_j.  The
 // division's reciprocal depends on r_jj only, so it is prepared for all j
@@ -650,7 +787,29 @@ static int mgs_mode(int nc) {
   if (v && strcmp(v, "sweeps") == 0) return 2;
   if (v && strcmp(v, "dataflow") == 0) return 1;
   if (v && strcmp(v, "flow") == 0) return 0;
+  if (v && strcmp(v, "warp") == 0) return 3;
   return nc == 4 ? 0 : 1;
+}
+
+// warp-per-column schedule when every column owner fits on the GPU at once
+template <class E, int R>
+static bool try_mgs_warp(int m, int n, double *A, double *Q, double *R_, MgsWork &w, cudaStream_t st) {
+  constexpr int es = Traits<E>::es;
+  const size_t smem = (size_t)es * R * 32 * sizeof(double);
+  auto kern = k_mgs_warp<E, R>;
+  if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem));
+  if ((long long)per_sm * num_sms() < n + 1) return false;
+  MgsStatus *status = w.status.as<MgsStatus>();
+  w.ready.ensure((size_t)(n + 1) * sizeof(int));
+  PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+  int *ready = w.ready.as<int>();
+  const double eps = level_eps(Traits<E>::nc);
+  void *args[] = {&A, &m, &n, (void *)&eps, &Q, &R_, &status, &ready};
+  PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, n + 1, 32, args, smem, st));
+  count_launch(1);
+  return true;
 }
 
 template <class E, int B>
@@ -660,6 +819,14 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
   const double eps = level_eps(Traits<E>::nc);
   const int sms = num_sms();
   const int mode = mgs_mode(Traits<E>::nc);
+  if (mode == 3 && Traits<E>::nc <= 2 && m <= 1024) {
+    bool done = false;
+    if (m <= 128) done = try_mgs_warp<E, 4>(m, n, A, Q, R, w, st);
+    else if (m <= 256) done = try_mgs_warp<E, 8>(m, n, A, Q, R, w, st);
+    else if (m <= 512) done = try_mgs_warp<E, 16>(m, n, A, Q, R, w, st);
+    else done = try_mgs_warp<E, 32>(m, n, A, Q, R, w, st);
+    if (done) return;
+  }
   if (mode == 0) {
     constexpr int NT = kMgsThreads;
     const size_t smem = (size_t)Traits<E>::es * NT * B * sizeof(double);

@@ -186,9 +186,9 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp"])
 def mgs_mode(request, monkeypatch):
-    """Both MGS schedules (persistent dataflow kernel, launch per sweep)."""
+    """Every MGS schedule (priority flow, dataflow, launch per sweep, warp per column)."""
     monkeypatch.setenv("PN_MGS_MODE", request.param)
     return request.param
 
