@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0,
                     help="config C5: number of homotopy start points (use with --dim 256 --terms 256 --base dd)")
     ap.add_argument("--max-iters", type=int, default=8)
+    ap.add_argument("--converge", action="store_true",
+                    help="config C4: run_newton to convergence (homotopy start t=0.99 when square; planted "
+                         "solution t=1 with x0 = z(1+1e-6u) when --rows > --dim)")
     return ap.parse_args()
 
 
@@ -461,10 +464,76 @@ def run_batched(args):
     dist.destroy_process_group()
 
 
+def run_converge(args):
+    """Config C4: full Gauss-Newton (run_newton, newton.py:106-132) on the
+    device-resident step until the reference's tolerance is met."""
+    import torch
+    torch.cuda.set_device(0)
+    from paper_1402_2626_b200 import _lib
+    from paper_1402_2626_b200.batch import homotopy_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem
+    from paper_1402_2626_b200.generators import random_sparse_system
+    from paper_1402_2626_b200.newton import NewtonConfig, run_newton
+    from paper_1402_2626_b200.xprec import precision_level
+
+    _lib.require_gpu()
+    level = precision_level(args.base, True)
+    n = args.dim
+    m = args.rows or n
+    packed = random_sparse_system(n, args.terms, args.k, level, seed=args.seed, m=m)
+    rng = np.random.default_rng(args.seed + 3)
+    theta = rng.uniform(0.0, 2.0 * math.pi, n)
+    z = np.zeros(level.cshape + (n,))
+    z[0, 0], z[1, 0] = np.cos(theta), np.sin(theta)
+    planted = m > n
+    t = level.from_float(1.0 if planted else 0.99)
+    t0 = time.perf_counter()
+    system, consts = homotopy_batch(packed, z[..., None, :], t)
+    # bake the start's constants into the system (B = 1 batch helper does the shift on the GPU)
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    coef = system.coeffs.reshape(level.es, -1).copy()
+    ks = np.diff(system.mon_ptr)
+    for i in range(m):
+        lo, hi = system.poly_ptr[i], system.poly_ptr[i + 1]
+        c = lo + int(np.nonzero(ks[lo:hi] == 0)[0][0])
+        coef[:, c] = consts.reshape(level.es, m)[:, i]
+    shifted = PackedSystem(level, n, system.poly_ptr, system.mon_ptr, system.var_idx, system.exps,
+                           np.ascontiguousarray(coef.reshape(system.coeffs.shape)))
+    del packed, system
+    prep = PreparedSystem(shifted)
+    t_setup = time.perf_counter() - t0
+    x0 = z.copy()
+    if planted:
+        x0[0, 0] *= 1.0 + 1e-6 * rng.uniform(-1, 1, n)
+        x0[1, 0] *= 1.0 + 1e-6 * rng.uniform(-1, 1, n)
+    cfg = NewtonConfig(level=level, max_iters=args.max_iters)
+    run_newton(prep, x0, NewtonConfig(level=level, max_iters=1))  # warm-up (first-touch allocations)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    w0 = time.perf_counter()
+    tr = run_newton(prep, x0, cfg)
+    wall = time.perf_counter() - w0
+    clk = clocks.stop()
+    gpu_s = tr.timings["evaluate"] + tr.timings["solve"] + tr.timings["update"]
+    print(json.dumps({
+        "metric": "Gauss-Newton run to convergence (config C4)", "value": wall, "unit": "s",
+        "higher_is_better": False, "n_gpus": 1, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"F({n},{args.terms},{args.k}) complex {args.base}, {m}x{n}, "
+                               + ("planted solution t=1, x0=z(1+1e-6u)" if planted else "homotopy start t=0.99, x0=z"),
+                   "m": m, "n": n},
+        "iterations": len(tr.entries), "converged": tr.converged,
+        "f_norm": [e.f_norm for e in tr.entries], "dx_norm": [e.dx_norm for e in tr.entries],
+        "gpu_seconds": gpu_s, "ms_per_step": 1e3 * gpu_s / max(1, len(tr.entries)),
+        "phases_s": tr.timings, "setup_s": t_setup, "clocks": clk}))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.converge:
+        run_converge(args)
     elif args.batch:
         run_batched(args)
     else:

@@ -812,6 +812,27 @@ static bool try_mgs_warp(int m, int n, double *A, double *Q, double *R_, MgsWork
   return true;
 }
 
+template <class E, int B, int NT>
+static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
+  MgsStatus *status = w.status.as<MgsStatus>();
+  double *orig = w.orig.d();
+  const double eps = level_eps(Traits<E>::nc);
+  const size_t smem = (size_t)Traits<E>::es * NT * B * sizeof(double);
+  auto kern = k_mgs_flow<E, B, NT>;
+  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  const int grid = std::min(per_sm * num_sms(), n + 1);
+  if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
+  w.ready.ensure((size_t)(n + 1) * sizeof(int));
+  PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+  int *ready = w.ready.as<int>();
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+  PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
+  count_launch(1);
+  return true;
+}
+
 template <class E, int B>
 static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
   MgsStatus *status = w.status.as<MgsStatus>();
@@ -828,22 +849,12 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     if (done) return;
   }
   if (mode == 0) {
-    constexpr int NT = kMgsThreads;
-    const size_t smem = (size_t)Traits<E>::es * NT * B * sizeof(double);
-    auto kern = k_mgs_flow<E, B, NT>;
-    PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-    const int grid = std::min(per_sm * sms, n + 1);
-    if (per_sm > 0 && (n + 1 + grid - 1) / grid <= 64) {
-      w.ready.ensure((size_t)(n + 1) * sizeof(int));
-      PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
-      int *ready = w.ready.as<int>();
-      void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
-      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
-      count_launch(1);
-      return;
+    // 6 warps x 8 rows for 1024 < m <= 1536 (the C4 overdetermined shape):
+    // a 96 KB column, two CTAs per SM instead of one 128 KB CTA
+    if constexpr (B == 8) {
+      if (m <= 1536 && flow_launch<E, B, 192>(m, n, A, Q, R, w, st)) return;
     }
+    if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
   if (mode <= 1) {
     int per_sm = 0;
