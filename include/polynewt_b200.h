@@ -16,6 +16,9 @@
  *   pn_back_substitute       <- mgs.back_substitute(_staged) (mgs.py:229-289)
  *   pn_least_squares         <- mgs.least_squares_solve    (mgs.py:299-305)
  *   pn_newton_step           <- newton.newton_step         (newton.py:82-103)
+ *   pn_newton_batch          <- newton.run_newton over homotopy_start_system
+ *                               starts                     (newton.py:106-159)
+ *   pn_residual_check        <- mgs.residual_check         (mgs.py:311-357)
  *
  * Conventions
  *  - A precision level is (nc, cplx): nc in {1,2,4} binary64 components
@@ -148,6 +151,14 @@ int pn_back_substitute(int nc, int cplx, int32_t n, const double *R, double *x, 
 /* x: planes (cshape, n); z receives hi(R[n,n]); Q, R optional as above. */
 int pn_least_squares(int nc, int cplx, int32_t m, int32_t n, const double *aug, double *x, double *z,
                      double *Q, double *R, pn_numinfo *info, void *stream);
+
+/* max componentwise |A - QR| recomputed in the next precision (d -> dd,
+ * dd -> qd), bit-identical to mgs.residual_check.  A, Q: planes (cshape, m, n);
+ * R: planes (cshape, n, n) (the leading block of the augmented factor).
+ * Quad-double factorisations return PN_E_ARG (the reference uses 320-bit
+ * mpfr there). */
+int pn_residual_check(int nc, int cplx, int32_t m, int32_t n, const double *A, const double *Q, const double *R,
+                      double *out, void *stream);
 
 /* ---- Newton ---------------------------------------------------------------- */
 /* One Gauss-Newton correction at x (planes (cshape, n)):

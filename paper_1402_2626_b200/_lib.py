@@ -77,6 +77,9 @@ SIGNATURES = {
     "pn_least_squares": ([ctypes.c_int, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                           ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p, ctypes.c_void_p,
                           ctypes.POINTER(NumInfo), ctypes.c_void_p], ctypes.c_int),
+    "pn_residual_check": ([ctypes.c_int, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                           ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p],
+                          ctypes.c_int),
     "pn_newton_step": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(NumInfo), ctypes.c_void_p],
                        ctypes.c_int),

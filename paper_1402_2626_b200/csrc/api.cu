@@ -182,3 +182,18 @@ extern "C" int pn_least_squares(int nc, int cplx, int32_t m, int32_t n, const do
   if (info) info->z = zhi;
   PN_API_END
 }
+
+// residual_check (mgs.py:311-357) for d and dd factorisations
+extern "C" int pn_residual_check(int nc, int cplx, int32_t m, int32_t n, const double *A, const double *Q,
+                                 const double *R, double *out, void *stream) {
+  PN_API_BEGIN
+  check_level(nc, cplx);
+  PN_REQUIRE(A && Q && R && out && m >= n && n >= 1, PN_E_ARG, "pn_residual_check: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int es = nc * (cplx ? 2 : 1);
+  DevIn da(A, (size_t)m * n * es, st), dq(Q, (size_t)m * n * es, st), dr(R, (size_t)n * n * es, st);
+  double r = 0.0;
+  dispatch_level(nc, cplx, [&]<class E>() { r = residual_impl<E>(m, n, da.d, dq.d, dr.d, st); });
+  *out = r;
+  PN_API_END
+}

@@ -209,6 +209,8 @@ void solve_batch_impl(int nb, const int32_t *slots, int m, int n, double *A, lon
                       double *R, long long Rs, double *x, long long xs, double *dx, double tol, int32_t *flags,
                       cudaStream_t st);
 template <class E>
+double residual_impl(int m, int n, const double *A, const double *Q, const double *R, cudaStream_t st);
+template <class E>
 void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st);
 template <class E>
 void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st);

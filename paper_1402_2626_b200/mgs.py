@@ -194,3 +194,24 @@ def least_squares_solve(aug: AugmentedMatrix, cfg: TilingConfig = TilingConfig()
                                       _lib.ptr(R), ctypes.byref(info), None)
     _lib.check(rc, info)
     return LeastSquaresResult(x=x, z=float(z.value), factors=QRFactors(ctx, Q, R))
+
+
+def residual_check(A: np.ndarray, Q: np.ndarray, R: np.ndarray, level) -> float:
+    """max componentwise |A - QR| in the next-higher precision (mgs.py:311-357).
+
+    d and dd factorizations are re-checked on the GPU in dd and qd arithmetic
+    with the reference's operation order, so the result is the reference's
+    float bit for bit.  R may be the (n+1)x(n+1) augmented factor; only its
+    leading n x n block is used.  Quad-double factorizations are checked in
+    320-bit mpfr by the reference; that has no GPU equivalent here and raises
+    ValueError."""
+    n = Q.shape[-1]
+    m = Q.shape[-2]
+    a = np.ascontiguousarray(A[..., :m, :n], dtype=np.float64)
+    q = np.ascontiguousarray(Q, dtype=np.float64)
+    r = np.ascontiguousarray(R[..., :n, :n], dtype=np.float64)
+    out = ctypes.c_double(0.0)
+    rc = _lib.load().pn_residual_check(level.ncomp, int(level.cplx), m, n, _lib.ptr(a), _lib.ptr(q), _lib.ptr(r),
+                                       ctypes.byref(out), None)
+    _lib.check(rc)
+    return float(out.value)

@@ -327,3 +327,31 @@ def test_homotopy_start_system_golden(gpu, name):
     for key in ("poly_ptr", "mon_ptr", "var_idx", "exps"):
         assert np.array_equal(getattr(s, key), g["shifted_" + key]), key
     assert same(s.coeffs, g["shifted_coeffs"])
+
+
+# -- residual_check (mgs.py:311-357) -----------------------------------------------------
+
+def _residual_goldens():
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "residuals.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", sorted(_residual_goldens()))
+def test_residual_check_golden(gpu, name):
+    """GPU residual_check (next precision, GEMM-tiled) == the reference's float."""
+    from paper_1402_2626_b200.mgs import residual_check
+    g = golden(name)
+    level = level_from_name(str(g["level"]))
+    n = g["Q"].shape[-1]
+    got = residual_check(g["aug"][..., :, :n], g["Q"], g["R"], level)
+    assert got == _residual_goldens()[name]
+
+
+def test_residual_check_qd_is_refused(gpu):
+    from paper_1402_2626_b200.mgs import residual_check
+    g = golden("mgs_24x13_cqd")
+    with pytest.raises(ValueError):
+        residual_check(g["aug"][..., :, :13], g["Q"], g["R"], level_from_name("cqd"))
