@@ -391,64 +391,94 @@ struct Pairwise {
 template <int B> struct Depth { static constexpr int value = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 3 : B <= 8 ? 4 : 5; };
 
 template <class E, int B, int NT>
-__global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
                                                     MgsStatus *status, int *ready) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) double smem_col[];
-  __shared__ E sme[NT / 32];
-  __shared__ Rl smr[NT / 32];
-  __shared__ int s_done[64];
-  __shared__ int s_known, s_fail, s_res;
+  // Broadcast slots are double-buffered by a CTA-uniform parity `par`: a slot
+  // written by use #a is only rewritten by use #a+2, and every thread has
+  // passed use #a+1's barrier (after reading #a) by then -- so a reduction
+  // needs two barriers instead of three, and the pivot poll rides along.
+  __shared__ E s_pe[2][NW], s_re[2];
+  __shared__ Rl s_pr[2][NW], s_rr[2];
+  __shared__ int s_kn[2], s_fl[2];
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
   const int row0 = tid * B;
   const int nparts = (m + B - 1) / B;
   const int nown = cta <= n ? (n - cta) / G + 1 : 0;
   const SmemCol<E, B> col{smem_col, NT * B};
   if (nown == 0) return;
-  if (tid == 0) {
-    s_known = 0;
-    s_fail = 0;
-    s_res = -1;
-  }
-  for (int i = tid; i < nown && i < 64; i += NT) s_done[i] = 0;
-  __syncthreads();
+  // CTA-uniform state (every thread holds the same values) and thread 0's
+  // private poll cursor
+  int known = 0, fail = 0, par = 0, res = -1;
+  int kn0 = 0, f0 = 0;
+  int done[64];
+  for (int i = 0; i < 64; ++i) done[i] = 0;
 
-  // load / store the resident column (coalesced over elements)
-  auto load_col = [&](int j) {
-    const double *g = A + (long long)j * m * es;
-    for (int r = tid; r < m; r += NT) col.put(r, eload<E>(g + (long long)r * es));
+  auto t0_poll = [&]() {  // thread 0: advance past every published pivot
+    while (kn0 < n && ld_acquire(ready + kn0)) ++kn0;
+    if (ld_acquire(&status->code)) f0 = 1;
   };
-  auto store_col = [&](int j) {
-    double *g = A + (long long)j * m * es;
-    for (int r = tid; r < m; r += NT) estore(g + (long long)r * es, col.get(r));
+  auto poll = [&]() {  // one barrier
+    if (tid == 0) {
+      t0_poll();
+      s_kn[par] = kn0;
+      s_fl[par] = f0;
+    }
+    __syncthreads();
+    known = s_kn[par];
+    fail = s_fl[par];
+    par ^= 1;
+  };
+  // tree_sum over the CTA's row blocks (two barriers, poll included)
+  auto reduce2 = [&](auto v, auto *part, auto *out) {
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const auto o = eshfl_down(v, s);
+      if ((lane & (2 * s - 1)) == 0 && tid + s < nparts) v = eadd(v, o);
+    }
+    if (lane == 0) part[par * NW + w] = v;
+    if (tid == 0) {
+      t0_poll();
+      s_kn[par] = kn0;
+      s_fl[par] = f0;
+    }
+    __syncthreads();
+    if (w == 0) {
+      const int nw = (nparts + 31) / 32;
+      auto x = part[par * NW + (lane < NW ? lane : 0)];
+#pragma unroll
+      for (int s = 1; s < NW; s <<= 1) {
+        const auto o = eshfl_down(x, s);
+        if ((lane & (2 * s - 1)) == 0 && lane + s < nw) x = eadd(x, o);
+      }
+      if (lane == 0) out[par] = x;
+    }
+    __syncthreads();
+    const auto r = out[par];
+    known = s_kn[par];
+    fail = s_fl[par];
+    par ^= 1;
+    return r;
   };
   auto make_resident = [&](int idx) {
-    if (s_res != idx) {
-      __syncthreads();
-      if (s_res >= 0) store_col(cta + s_res * G);
-      __syncthreads();
-      load_col(cta + idx * G);
-      __syncthreads();
-      if (tid == 0) s_res = idx;
-      __syncthreads();
+    if (res == idx) return;
+    __syncthreads();  // the current column's sweeps are done with the smem rows
+    if (res >= 0) {
+      double *g = A + (long long)(cta + res * G) * m * es;
+      for (int r = tid; r < m; r += NT) estore(g + (long long)r * es, col.get(r));
     }
-  };
-  // advance the CTA-wide count of published pivots (non-blocking)
-  auto poll = [&]() {
+    const double *g = A + (long long)(cta + idx * G) * m * es;
+    for (int r = tid; r < m; r += NT) col.put(r, eload<E>(g + (long long)r * es));
     __syncthreads();
-    if (tid == 0) {
-      int kn = s_known;
-      while (kn < n && ld_acquire(ready + kn)) ++kn;
-      s_known = kn;
-      if (ld_acquire(&status->code)) s_fail = 1;
-    }
-    __syncthreads();
+    res = idx;
   };
   auto block_wait = [&](int k) {
-    __syncthreads();
     if (tid == 0) {
       long long t0 = clock64();
       while (!ld_acquire(ready + k)) {
@@ -472,7 +502,7 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
       const int r = row0 + q;
       if (r < m) pw.push(emul(econj(eload_cg<E>(qk + (long long)r * es)), col.get(r)));
     }
-    const E rk = block_tree_reduce<E, NT>(pw.fold(), nparts, sme);
+    const E rk = reduce2(pw.fold(), &s_pe[0][0], s_re);
 #pragma unroll
     for (int q = 0; q < B; ++q) {
       const int r = row0 + q;
@@ -486,7 +516,7 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
 #pragma unroll
     for (int q = 0; q < B; ++q)
       if (row0 + q < m) pw.push(eabs2(col.get(row0 + q)));
-    return fsqrt(block_tree_reduce<Rl, NT>(pw.fold(), nparts, smr));
+    return fsqrt(reduce2(pw.fold(), &s_pr[0][0], s_rr));
   };
 
   // phase 0: initial norms of the owned columns (mgs.py:171-172)
@@ -498,17 +528,17 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
     if (tid == 0) orig[j] = nrm.c[0];
   }
 
+  poll();
   int lo = 0;
   while (lo < nown) {
     const int c = cta + lo * G;
-    poll();
-    if (s_fail) return;
-    int dlo = s_done[lo];
-    if (dlo < c && dlo >= s_known) {
+    if (fail) return;
+    const int dlo = done[lo];
+    if (dlo < c && dlo >= known) {
       // critical column blocked on pivot dlo: catch a lagging column up
       int pick = -1;
       for (int i = lo + 1; i < nown; ++i)
-        if (s_done[i] < s_known) {
+        if (done[i] < known) {
           pick = i;
           break;
         }
@@ -518,34 +548,29 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
       }
       make_resident(pick);
       const int cj = cta + pick * G;
-      int d = s_done[pick];
-      while (d < s_known && d < cj) {
+      int d = done[pick];
+      while (d < known && d < cj) {
         apply(d, cj);
         ++d;
-        poll();
-        if (s_fail) return;
-        if (s_known > s_done[lo]) break;  // the critical column can move again
+        if (fail) return;
+        if (known > dlo) break;  // the critical column can move again
       }
-      __syncthreads();
-      if (tid == 0) s_done[pick] = d;
-      __syncthreads();
+      done[pick] = d;
       continue;
     }
     // serve the critical column with every published sweep
     make_resident(lo);
     int d = dlo;
     while (d < c) {
-      if (d >= s_known) {
+      if (d >= known) {
         poll();
-        if (s_fail) return;
-        if (d >= s_known) break;  // next pivot not out yet: reconsider the work list
+        if (fail) return;
+        if (d >= known) break;  // next pivot not out yet: reconsider the work list
       }
       apply(d, c);
       ++d;
     }
-    __syncthreads();
-    if (tid == 0) s_done[lo] = d;
-    __syncthreads();
+    done[lo] = d;
     if (d < c) continue;
     // pivot c (mgs.py:176-193); c == n is the residual norm z
     const Rl rkk = norm();
@@ -569,9 +594,10 @@ __global__ void __launch_bounds__(NT, 2) k_mgs_flow(double *__restrict__ A, int 
       double *qc = Q + (long long)c * m * es;
       for (int r = tid; r < m; r += NT) estore(qc + (long long)r * es, ediv_prepared(col.get(r), p));
       publish(ready, c);
+    } else {
+      __syncthreads();
     }
-    __syncthreads();
-    if (tid == 0) s_res = -1;  // column c is final; nothing to write back
+    res = -1;  // column c is final; nothing to write back
     ++lo;
   }
 }
@@ -993,11 +1019,170 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Lane-parallel back substitution for complex quad double.  The solve is a
+// chain of n dependent complex-qd operations; a single lane issues a complex
+// multiply in ~4300 cycles (profiles/r01/micro_fp64.txt) because its four
+// qd products share one instruction stream.  Here four lanes own a row and
+// compute the four real products of every complex multiply side by side
+// (then two lanes form re = t1 - t2 and im = t3 + t4), which shortens the
+// chain about 2.5x.  The reference's operation sequence is unchanged
+// (xprec.py:302-306, varith.py:130-136), so x is bit-identical.
+//
+// Layout: CTA 0 (128 threads = 32 rows x 4 lanes) solves each 32-row
+// diagonal block and then applies the block's x to the next block's rows;
+// the rest of the grid updates all rows above that, one lane per row, with
+// one grid barrier per block (as k_backsub_blocked).
+
+__device__ __forceinline__ F<4> shfl_f4(const F<4> &v, int src) {
+  F<4> r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r.c[i] = __shfl_sync(0xffffffffu, v.c[i], src);
+  return r;
+}
+__device__ __forceinline__ F<4> shfl_xor_f4(const F<4> &v, int mask) {
+  F<4> r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r.c[i] = __shfl_xor_sync(0xffffffffu, v.c[i], mask);
+  return r;
+}
+// a*b on a group of four lanes (p = lane & 3): p0 ar*br, p1 ai*bi, p2 ar*bi,
+// p3 ai*br; re = t1 - t2 on p0, im = t3 + t4 on p2.  Every lane of the warp
+// must call it (full-mask shuffles); all four lanes get the result.
+__device__ __forceinline__ C<4> lp_cmul(const C<4> &a, const C<4> &b, int p, int g4) {
+  const F<4> x = (p == 0 || p == 2) ? a.re : a.im;
+  const F<4> y = (p == 0 || p == 3) ? b.re : b.im;
+  const F<4> prod = qd_mul_call(x, y);
+  const F<4> other = shfl_xor_f4(prod, 1);
+  const F<4> v = qd_add_call(prod, p == 0 ? fneg(other) : other);
+  return {shfl_f4(v, g4), shfl_f4(v, g4 + 2)};
+}
+// a - b: p0 re, p1 im
+__device__ __forceinline__ C<4> lp_csub(const C<4> &a, const C<4> &b, int p, int g4) {
+  const F<4> v = qd_add_call((p & 1) ? a.im : a.re, fneg((p & 1) ? b.im : b.re));
+  return {shfl_f4(v, g4), shfl_f4(v, g4 + 1)};
+}
+// y / r as (y * conj r) * recip(|r|^2) (varith.py:130-136 with the hoisted reciprocal)
+__device__ __forceinline__ C<4> lp_div(const C<4> &yv, const C<4> &r, const RDiv<4> &pr, int p, int g4) {
+  const C<4> num = lp_cmul(yv, cconj(r), p, g4);
+  const F<4> v = qd_mul_call((p & 1) ? num.im : num.re, pr.v);
+  return {shfl_f4(v, g4), shfl_f4(v, g4 + 1)};
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_backsub_lanes(const double *__restrict__ R, int n, double *__restrict__ x,
+                                                      RDiv<4> *__restrict__ prep, double *__restrict__ y,
+                                                      int *sing, MgsStatus *status) {
+  namespace cg = cooperative_groups;
+  using E = C<4>;
+  constexpr int es = 8;
+  static_assert(NT == 128, "CTA 0 is 32 rows x 4 lanes");
+  extern __shared__ __align__(16) double bl_smem[];
+  E *sD = reinterpret_cast<E *>(bl_smem);  // 32 x 32 diagonal block, column-major
+  E *sU = sD + 32 * 32;                     // 32 x 32 block above it
+  E *sX = sU + 32 * 32;                     // x of the current block
+  RDiv<4> *sP = reinterpret_cast<RDiv<4> *>(sX + 32);
+  cg::grid_group grid = cg::this_grid();
+  if (status->code) return;
+  const long long ld = n + 1;
+  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
+  for (int j = gtid; j < n; j += gsize) {
+    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
+    const double *dg = R + ((long long)j * ld + j) * es;
+    bool nz = false;
+#pragma unroll
+    for (int q = 0; q < es; ++q) nz |= dg[q] != 0.0;
+    if (!nz) atomicMax(sing, j);
+    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
+  }
+  grid.sync();
+  if (*(volatile int *)sing >= 0) {
+    if (gtid == 0) {
+      status->k = *sing;
+      status->code = PN_E_SINGULAR;
+    }
+    return;
+  }
+  const bool solver = blockIdx.x == 0;
+  const int t = threadIdx.x, lane = t & 31, p = lane & 3, g4 = lane & ~3;
+  const int rl = t >> 2;  // solver row within the block
+  const int nb = (n + 31) / 32;
+  for (int b = nb - 1; b >= 0; --b) {
+    const int lo = b * 32, hi = min(n, lo + 32), nbk = hi - lo;
+    if (solver) {
+      for (int e = t; e < 32 * 32; e += NT) {
+        const int jj = e >> 5, ii = e & 31;
+        if (jj < nbk && ii <= jj) sD[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo + ii) * es);
+      }
+      if (t < nbk) sP[t] = prep[lo + t];
+      __syncthreads();
+      E yr = rl < nbk ? eload<E>(y + (long long)(lo + rl) * es) : ezero<E>();
+      for (int j = hi - 1; j >= lo; --j) {
+        const int jl = j - lo;
+        if ((jl >> 3) == (t >> 5)) {  // the warp holding row jl divides (all its lanes shuffle)
+          const E xj = lp_div(yr, sD[jl * 32 + jl], sP[jl], p, g4);
+          if (rl == jl && p == 0) sX[jl] = xj;
+        }
+        __syncthreads();
+        if ((t >> 5) * 8 < jl) {  // warps with a row below jl update
+          const E u = lp_csub(yr, lp_cmul(sD[jl * 32 + rl], sX[jl], p, g4), p, g4);
+          if (rl < jl) yr = u;
+        }
+      }
+      __syncthreads();
+      if (t < nbk) estore(x + (long long)(lo + t) * es, sX[t]);
+    }
+    grid.sync();  // x of block b is visible to every CTA
+    if (b == 0) break;
+    if (solver) {
+      // the next block's rows take this block's x, in descending column order
+      const int r = lo - 32 + rl;
+      for (int e = t; e < 32 * 32; e += NT) {
+        const int jj = e >> 5, ii = e & 31;
+        if (jj < nbk) sU[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + ii) * es);
+      }
+      __syncthreads();
+      E v = eload<E>(y + (long long)r * es);
+      for (int j = hi - 1; j >= lo; --j) v = lp_csub(v, lp_cmul(sU[(j - lo) * 32 + rl], sX[j - lo], p, g4), p, g4);
+      if (p == 0) estore(y + (long long)r * es, v);
+      __syncthreads();
+    } else {
+      // all rows above the next block take this block's x
+      for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {
+        E v = eload<E>(y + (long long)r * es);
+        for (int j = hi - 1; j >= lo; --j)
+          v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+        estore(y + (long long)r * es, v);
+      }
+    }
+  }
+}
+
 template <class E>
 void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st) {
   constexpr int es = Traits<E>::es;
   DevBuf prep((size_t)n * Traits<E>::nc * sizeof(double) + 16, st);
   const char *mode = getenv("PN_BACKSUB_MODE");
+  if constexpr (std::is_same_v<E, C<4>>) {
+    if (!(mode && (strcmp(mode, "single") == 0 || strcmp(mode, "blocked") == 0))) {
+      constexpr int NT = 128;
+      DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
+      DevBuf sbuf(16, st);
+      int *sing = sbuf.as<int>();
+      PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
+      const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
+      RDiv<4> *pp = prep.as<RDiv<4>>();
+      double *yp = yw.d();
+      MgsStatus *status = w.status.as<MgsStatus>();
+      void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
+      const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<4>);
+      PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_lanes<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_lanes<NT>, grid, NT, args, smem, st));
+      count_launch(1);
+      return;
+    }
+  }
   if (!(mode && strcmp(mode, "single") == 0)) {
     constexpr int NT = 128;
     DevBuf yw((size_t)n * es * sizeof(double) + 16, st);

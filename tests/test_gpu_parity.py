@@ -254,8 +254,8 @@ def test_breakdown_mid_factorisation_vs_oracle(gpu, mgs_mode, lv):
     assert (got.value.k, got.value.rkk, got.value.threshold) == (want.value.k, want.value.rkk, want.value.threshold)
 
 
-@pytest.mark.parametrize("bmode", ["blocked", "single"])
-@pytest.mark.parametrize("lv,n", [("cqd", 77), ("cdd", 1000), ("rd", 33), ("cd", 1500), ("rqd", 64)])
+@pytest.mark.parametrize("bmode", ["lanes", "blocked", "single"])
+@pytest.mark.parametrize("lv,n", [("cqd", 77), ("cqd", 300), ("cdd", 1000), ("rd", 33), ("cd", 1500), ("rqd", 64)])
 def test_back_substitution_vs_oracle(gpu, monkeypatch, bmode, lv, n):
     from paper_1402_2626_b200.mgs import back_substitute
     from paper_1402_2626_b200.varith import VecContext
@@ -275,10 +275,11 @@ def test_back_substitution_vs_oracle(gpu, monkeypatch, bmode, lv, n):
     assert same(got, oracle.back_substitute(L, Ra))
 
 
-def test_singular_back_substitution(gpu):
+@pytest.mark.parametrize("lv", ["cdd", "cqd"])
+def test_singular_back_substitution(gpu, lv):
     from paper_1402_2626_b200.mgs import SingularMatrixError, back_substitute
     from paper_1402_2626_b200.varith import VecContext
-    ctx = VecContext(level_from_name("cdd"))
+    ctx = VecContext(level_from_name(lv))
     R = np.zeros(ctx.cshape + (4, 4))
     R[0, 0] = np.eye(4)
     R[0, 0, 2, 2] = 0.0
