@@ -66,20 +66,37 @@ def level_costs(nc: int, cplx: bool):
     return {"add": radd, "mul": rmul, "int": rmul, "radd": radd, "rmul": rmul}
 
 
-def work_counts(stats, nc: int, cplx: bool, m: int, n: int):
+def committed_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of `kernel` on `workload` from the newest
+    committed ncu capture (profiles/*/traffic.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                rec = json.load(f).get(f"{kernel} | {workload}")
+        except (OSError, ValueError):
+            continue
+        if rec:
+            return rec["dram_read_bytes"] + rec["dram_write_bytes"]
+    return None
+
+
+def work_counts(stats, nc: int, cplx: bool, m: int, n: int, split: bool = False):
     """Algorithmic FP64 instruction counts and bytes of one step."""
     c = level_costs(nc, cplx)
     w_eval = (stats.mul_ops * c["mul"] + stats.int_mul_ops * c["int"] + stats.add_ops * c["add"]
               + stats.table_mul_ops * c["mul"])
     U = m * n * (n + 1) // 2                      # MGS update elements
-    w_mgs = (U * (2 * c["mul"] + 2 * c["add"])    # r_kj dot + a -= q r
-             + (2 * n + 1) * m * (2 * c["rmul"] + 2 * c["radd"]) // (1 if cplx else 2)  # norms
-             + n * m * (2 if cplx else 1) * c["rmul"]                                    # q = a / r
-             + n * (n - 1) // 2 * (c["mul"] + c["add"]))                                 # back-sub
+    w_factor = (U * (2 * c["mul"] + 2 * c["add"])    # r_kj dot + a -= q r
+                + (2 * n + 1) * m * (2 * c["rmul"] + 2 * c["radd"]) // (1 if cplx else 2)  # norms
+                + n * m * (2 if cplx else 1) * c["rmul"])                                   # q = a / r
+    w_bsub = n * (n - 1) // 2 * (c["mul"] + c["add"])                                       # back-sub
     es = nc * (2 if cplx else 1)
     b_eval = (stats.support * 8 + (stats.monomials + 1) * 4 + stats.monomials * es * 8
               + (n + m) * es * 8 + m * n * es * 8)
-    return w_eval, w_mgs, b_eval
+    if split:
+        return w_eval, w_factor, w_bsub, b_eval
+    return w_eval, w_factor + w_bsub, b_eval
 
 
 class ClockSampler:
@@ -240,7 +257,8 @@ def run_ours(args):
     prep = PreparedSystem(packed)
     t_prep = time.perf_counter() - t_prep
     stats = prep.stats()
-    w_eval, w_mgs, b_eval = work_counts(stats, nc, level.cplx, m, n)
+    w_eval, w_factor, w_bsub, b_eval = work_counts(stats, nc, level.cplx, m, n, split=True)
+    w_mgs = w_factor + w_bsub
 
     dev = torch.device("cuda", torch.cuda.current_device())
     x_d = torch.from_numpy(x_host).to(dev)
@@ -254,7 +272,7 @@ def run_ours(args):
                                 _lib.ptr(outs["dx"]), _lib.ptr(outs["fm"]), _lib.ptr(outs["dm"]),
                                 _lib.ptr(outs["xm"]), ctypes.byref(info), ctypes.c_void_p(stream))
         _lib.check(rc, info)
-        return info.t_evaluate, info.t_solve, info.t_update
+        return info.t_evaluate, info.t_solve, info.t_update, info.t_factor
 
     peak = ctypes.c_double(0)
     _lib.check(lib.pn_fp64_peak(ctypes.byref(peak), ctypes.c_void_p(stream)))
@@ -325,12 +343,18 @@ def run_ours(args):
     t_eval = statistics.median(p[0] for p in phases)
     t_solve = statistics.median(p[1] for p in phases)
     t_upd = statistics.median(p[2] for p in phases)
-    mgs_rate = w_mgs / t_solve
-    roofline = {"bound": "fp64", "kernel": "k_mgs_sweep (MGS least squares phase)",
+    t_fac = statistics.median(p[3] for p in phases)
+    mgs_rate = w_factor / t_fac
+    workload = f"F({args.dim},{args.terms},{args.k}) complex {args.base} {m}x{n}"
+    mgs_kernel = "k_mgs_flow" if nc == 4 else "k_mgs_dataflow"
+    roofline = {"bound": "fp64", "kernel": f"{mgs_kernel} (MGS factorisation of [J | -f], one launch per step)",
                 "achieved": mgs_rate / 1e12, "peak": fp64_peak / 1e12, "unit": "T FP64-instr/s",
-                "frac": mgs_rate / fp64_peak, "traffic": None,
+                "frac": mgs_rate / fp64_peak, "traffic": committed_traffic(mgs_kernel, workload),
                 "peak_source": "measured in-run DFMA probe (pn_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
-                "work_fp64_instr": w_mgs}
+                "work_fp64_instr": w_factor, "seconds": t_fac,
+                "arithmetic_ceiling_frac": {4: 0.76, 2: 0.95}.get(nc)}
+    bsub = {"kernel": "k_backsub_lanes" if nc == 4 else "k_backsub_blocked", "seconds": t_solve - t_fac,
+            "work_fp64_instr": w_bsub, "bound": "latency (n dependent divisions)"}
     evalr = {"kernel": "k_mono_tree + k_segments (eval+diff phase)", "seconds": t_eval,
              "achieved_fp64": w_eval / t_eval / 1e12, "frac_fp64": w_eval / t_eval / fp64_peak,
              "achieved_gbs": b_eval / t_eval / 1e9, "work_fp64_instr": w_eval, "bytes": b_eval}
@@ -356,6 +380,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": roofline,
             "eval_roofline": evalr,
+            "backsub": bsub,
             "phases_ms": {"evaluate": t_eval * 1e3, "solve": t_solve * 1e3, "update": t_upd * 1e3},
             "cpu_baseline": cpu,
             "clocks": clk,

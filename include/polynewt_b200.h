@@ -76,6 +76,7 @@ typedef struct {
   double t_evaluate; /* pn_newton_step phase times (seconds, CUDA events) */
   double t_solve;
   double t_update;
+  double t_factor;  /* MGS factorisation alone (part of t_solve), seconds */
 } pn_numinfo;
 
 /* OpCounter (evaldiff.py:21-30): multiplication tallies of one evaluation */

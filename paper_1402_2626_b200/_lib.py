@@ -36,7 +36,7 @@ _c_int64_p = ctypes.POINTER(ctypes.c_int64)
 class NumInfo(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("index", ctypes.c_int32), ("rkk", ctypes.c_double),
                 ("threshold", ctypes.c_double), ("z", ctypes.c_double), ("t_evaluate", ctypes.c_double),
-                ("t_solve", ctypes.c_double), ("t_update", ctypes.c_double)]
+                ("t_solve", ctypes.c_double), ("t_update", ctypes.c_double), ("t_factor", ctypes.c_double)]
 
 
 class Counts(ctypes.Structure):

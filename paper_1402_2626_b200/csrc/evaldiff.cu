@@ -279,8 +279,11 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
 // this path (pn_system::Fused); everything else uses K1 + K2.
 
 template <class E> struct TreeG;  // lanes per monomial, by precision
+#ifndef PN_TREE_G_DD
+#define PN_TREE_G_DD 4
+#endif
 template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
-template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
+template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : NC == 2 ? PN_TREE_G_DD : 4; };
 
 // binary-counter stack: level l of the stack lives at st[l * stride]
 template <class E>

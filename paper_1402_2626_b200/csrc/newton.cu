@@ -30,12 +30,12 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
   double *xa = sys->xbuf.d(), *A = sys->Abuf.d(), *fa = sys->fbuf.d();
   double *Q = sys->vbuf.d(), *R = sys->Rbuf.d(), *dxa = sys->xsol.d(), *xn = dxa + (size_t)n * es;
 
-  cudaEvent_t ev[4];
+  cudaEvent_t ev[5];
   for (auto &e : ev) PN_CHECK_CUDA(cudaEventCreate(&e));
   struct EvGuard {
     cudaEvent_t *e;
     ~EvGuard() {
-      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
     }
   } guard{ev};
   planes_to_aos(es, n, din.d, xa, st);
@@ -44,6 +44,7 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
   evaldiff_device(sys, xa, fa, A, m, n, st);
   PN_CHECK_CUDA(cudaEventRecord(ev[1], st));
   mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, st);
+  PN_CHECK_CUDA(cudaEventRecord(ev[4], st));
   backsub_device(nc, cplx, n, R, dxa, sys->mgs, st);
   PN_CHECK_CUDA(cudaEventRecord(ev[2], st));
   // x_next = x + dx (newton.py:92)
@@ -88,6 +89,9 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
     info->t_evaluate = ms[0] * 1e-3;
     info->t_solve = ms[1] * 1e-3;
     info->t_update = ms[2] * 1e-3;
+    float mf = 0.f;
+    PN_CHECK_CUDA(cudaEventElapsedTime(&mf, ev[1], ev[4]));
+    info->t_factor = mf * 1e-3;
   }
   PN_CHECK_CUDA(cudaStreamSynchronize(st));
   PN_API_END
