@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
 
 template <class E> struct TreeG;  // lanes per monomial, by precision
 #ifndef PN_TREE_G_DD
-#define PN_TREE_G_DD 4
+#define PN_TREE_G_DD 8  // cdd: 8 lanes per monomial (fewer registers, 3 CTAs/SM) measured faster than 4
 #endif
 template <int NC> struct TreeG<F<NC>> { static constexpr int value = NC == 4 ? 8 : 4; };
 template <int NC> struct TreeG<C<NC>> { static constexpr int value = NC == 4 ? 8 : NC == 2 ? PN_TREE_G_DD : 4; };
