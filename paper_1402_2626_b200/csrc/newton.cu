@@ -115,6 +115,14 @@ __global__ void k_scatter_consts(int m, const int32_t *__restrict__ cpos, const 
   if (i < m) estore(coeff + (long long)cpos[i] * es, eload<E>(src + (long long)i * es));
 }
 
+template <class E>
+__global__ void k_gather_consts(int m, const int32_t *__restrict__ cpos, const double *__restrict__ coeff,
+                                double *__restrict__ dst) {
+  constexpr int es = Traits<E>::es;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) estore(dst + (long long)i * es, eload<E>(coeff + (long long)cpos[i] * es));
+}
+
 // Python's math.fsum (CPython's msum with the half-even fix-up): the float()
 // of a quad double (xprec.py:261-262) used by the convergence test.
 double host_fsum(const double *v, int n) {
@@ -186,6 +194,16 @@ static void newton_batch_serial(pn_system *sys, int64_t B, const double *x0, con
   DevBuf mod((size_t)2 * n * nc * sizeof(double) + 16, st);
   std::vector<double> hmod((size_t)2 * n * nc);
   const double eps = nc == 1 ? 0x1p-53 : nc == 2 ? 0x1p-104 : 0x1p-209;
+  // the per-start constants are written into the system's coefficients;
+  // keep the originals and restore them afterwards (no side effect on sys)
+  DevBuf saved(consts ? (size_t)m * ebytes + 16 : 16, st);
+  if (consts) {
+    dispatch_level(nc, cplx, [&]<class E>() {
+      k_gather_consts<E><<<(m + 127) / 128, 128, 0, st>>>(m, cpos_d.as<int32_t>(), sys->d_coeff, saved.d());
+    });
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+  }
   for (int64_t b = 0; b < B; ++b) {
     double *xb = xa_all.d() + (size_t)b * n * es;
     if (consts) {
@@ -222,6 +240,13 @@ static void newton_batch_serial(pn_system *sys, int64_t B, const double *x0, con
     }
     iters[b] = it > max_iters ? max_iters : it;
     status[b] = stat;
+  }
+  if (consts) {
+    dispatch_level(nc, cplx, [&]<class E>() {
+      k_scatter_consts<E><<<(m + 127) / 128, 128, 0, st>>>(m, cpos_d.as<int32_t>(), saved.d(), sys->d_coeff);
+    });
+    PN_CHECK_LAUNCH();
+    count_launch(1);
   }
   DevOut xo(x_out, (size_t)B * n * es, st);
   if (B) aos_to_planes(es, B * n, xa_all.d(), xo.d, st);

@@ -185,3 +185,26 @@ def test_batch_breakdown_status(gpu):
     assert list(res.status) == [2] * B
     assert list(res.iters) == [1] * B
     assert same(res.x, Z)
+
+
+@pytest.mark.gpu
+def test_serial_batch_matches_slots_and_leaves_system_unchanged(gpu, monkeypatch):
+    """PN_BATCH_MODE=serial (one start at a time, also used for m > 1024)
+    gives the slot path's results and restores the system's constants."""
+    from paper_1402_2626_b200.batch import homotopy_batch, run_newton_batch
+    from paper_1402_2626_b200.evaldiff import PreparedSystem, evaluate_system
+    from paper_1402_2626_b200.generators import random_sparse_system, random_unit_point
+    level = level_from_name("cdd")
+    p = random_sparse_system(20, 6, 3, level, seed=21, maxexp=2)
+    B = 4
+    Z = np.stack([level.to_planes(random_unit_point(20, 300 + b, level)) for b in range(B)], axis=-2)
+    system, consts = homotopy_batch(p, Z, level.from_float(0.99))
+    prep = PreparedSystem(system)
+    z0 = np.ascontiguousarray(Z[..., 0, :])
+    before = evaluate_system(prep, z0).f
+    slots = run_newton_batch(prep, Z, consts, max_iters=6)
+    monkeypatch.setenv("PN_BATCH_MODE", "serial")
+    serial = run_newton_batch(prep, Z, consts, max_iters=6)
+    assert same(serial.x, slots.x)
+    assert np.array_equal(serial.iters, slots.iters) and np.array_equal(serial.status, slots.status)
+    assert same(evaluate_system(prep, z0).f, before)
