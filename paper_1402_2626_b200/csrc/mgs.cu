@@ -271,30 +271,80 @@ __global__ void __launch_bounds__(kMgsThreads) k_mgs_dataflow(double *__restrict
     finish_pivot<E, B>(v, row0, m, n, 0, rkk, orig, eps, Q, R, status);
     publish(ready, 0);
   }
-  for (int k = 0; k < n; ++k) {
-    // first owned column after k
-    int j0 = k + 1 + (((cta - (k + 1)) % G) + G) % G;
-    if (j0 > n) break;
-    if (!wait_pivot(ready, k, status)) return;
-    E qv[B];
-    load_rows_cg<E, B>(qv, Q + (long long)k * m * es, row0, m);
-    for (int j = j0; j <= n; j += G) {
-      double *col = A + (long long)j * m * es;
-      E a[B], pr[B];
-      load_rows<E, B>(a, col, row0, m);
-#pragma unroll
-      for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), a[q]);
-      E part = local_tree<E, B>(pr, valid);
-      const E r = block_tree_reduce<E, kMgsThreads>(part, nparts, sme);
-#pragma unroll
-      for (int q = 0; q < B; ++q) a[q] = esub(a[q], emul(qv[q], r));
-      store_rows<E, B>(col, a, row0, m);
-      if (threadIdx.x == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
-      if (j == k + 1) {
-        Rl rkk = column_norm<E, B>(a, row0, m, smr);
-        const bool ok = finish_pivot<E, B>(a, row0, m, n, k + 1, rkk, orig, eps, Q, R, status);
-        publish(ready, k + 1);  // also on breakdown, so that waiters wake up
-        if (!ok) return;
+  if constexpr (Traits<E>::nc == 1) {
+    // Every thread only ever reads back the rows it stored itself, so the next
+    // (sweep, column) pair's rows can be loaded while the current one computes
+    // (also across the wait for the next pivot); the L2 latency of the column
+    // load leaves the critical path.
+    auto first_after = [&](int k) { return k + 1 + (((cta - (k + 1)) % G) + G) % G; };
+    E cur[B];
+    int have = -1;  // column whose current rows are in cur
+    for (int k = 0; k < n; ++k) {
+      const int j0 = first_after(k);
+      if (j0 > n) break;
+      if (!wait_pivot(ready, k, status)) return;
+      E qv[B];
+      load_rows_cg<E, B>(qv, Q + (long long)k * m * es, row0, m);
+      for (int j = j0; j <= n; j += G) {
+        double *col = A + (long long)j * m * es;
+        if (have != j) load_rows<E, B>(cur, col, row0, m);
+        // next pair: (k, j+G) or (k+1, first column after k+1)
+        int jn = j + G;
+        if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
+        const bool pf = jn <= n && jn != j;
+        E nxt[B];
+        if (pf) load_rows<E, B>(nxt, A + (long long)jn * m * es, row0, m);
+        E pr[B];
+  #pragma unroll
+        for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), cur[q]);
+        E part = local_tree<E, B>(pr, valid);
+        const E r = block_tree_reduce<E, kMgsThreads>(part, nparts, sme);
+  #pragma unroll
+        for (int q = 0; q < B; ++q) cur[q] = esub(cur[q], emul(qv[q], r));
+        store_rows<E, B>(col, cur, row0, m);
+        if (threadIdx.x == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
+        if (j == k + 1) {
+          Rl rkk = column_norm<E, B>(cur, row0, m, smr);
+          const bool ok = finish_pivot<E, B>(cur, row0, m, n, k + 1, rkk, orig, eps, Q, R, status);
+          publish(ready, k + 1);  // also on breakdown, so that waiters wake up
+          if (!ok) return;
+        }
+        if (pf) {
+  #pragma unroll
+          for (int q = 0; q < B; ++q) cur[q] = nxt[q];
+          have = jn;
+        } else {
+          have = (jn == j) ? j : -1;  // the same column again next sweep: cur is current
+        }
+      }
+    }
+  } else {
+    // dd/qd: the prefetch registers would cost the second CTA per SM (measured slower)
+    for (int k = 0; k < n; ++k) {
+      // first owned column after k
+      int j0 = k + 1 + (((cta - (k + 1)) % G) + G) % G;
+      if (j0 > n) break;
+      if (!wait_pivot(ready, k, status)) return;
+      E qv[B];
+      load_rows_cg<E, B>(qv, Q + (long long)k * m * es, row0, m);
+      for (int j = j0; j <= n; j += G) {
+        double *col = A + (long long)j * m * es;
+        E a[B], pr[B];
+        load_rows<E, B>(a, col, row0, m);
+  #pragma unroll
+        for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), a[q]);
+        E part = local_tree<E, B>(pr, valid);
+        const E r = block_tree_reduce<E, kMgsThreads>(part, nparts, sme);
+  #pragma unroll
+        for (int q = 0; q < B; ++q) a[q] = esub(a[q], emul(qv[q], r));
+        store_rows<E, B>(col, a, row0, m);
+        if (threadIdx.x == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
+        if (j == k + 1) {
+          Rl rkk = column_norm<E, B>(a, row0, m, smr);
+          const bool ok = finish_pivot<E, B>(a, row0, m, n, k + 1, rkk, orig, eps, Q, R, status);
+          publish(ready, k + 1);  // also on breakdown, so that waiters wake up
+          if (!ok) return;
+        }
       }
     }
   }
