@@ -444,6 +444,82 @@ static void launch_fused(pn_system *sys, const double *x, const double *table, d
 }
 
 // ---------------------------------------------------------------------------
+// K1 with TMA-staged supports (dense uniform buckets: every monomial of the
+// bucket has k = K and the bucket's support entries are one contiguous block,
+// as for the C2/C4/C5 systems).  Persistent CTAs walk chunks of CH = NT/G
+// monomials; a chunk's variable indices, exponents, contribution slots and
+// canonical indices arrive in shared memory by cp.async.bulk on an mbarrier,
+// double buffered, so the next chunk's supports stream in while the current
+// chunk's trees compute and no lane waits on a dependent index load.  The
+// arithmetic is mono_tree_eval, identical to k_mono_tree.
+template <class E, int BASE, int G, int NT>
+__global__ void __launch_bounds__(NT) k_mono_tree_tma(const int32_t *__restrict__ list, long long count, int K,
+                                                      long long e0, const int32_t *__restrict__ var,
+                                                      const int32_t *__restrict__ exps,
+                                                      const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                                                      const double *__restrict__ x, const double *__restrict__ table,
+                                                      const int32_t *__restrict__ toff, double *__restrict__ contrib,
+                                                      BView bv) {
+  constexpr int es = Traits<E>::es;
+  constexpr int CH = NT / G;
+  extern __shared__ __align__(16) int tma_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int L = CH * K;                        // ints per array per stage (multiple of 4)
+  int *st_var = tma_smem;                      // [2][L]
+  int *st_exp = st_var + 2 * L;                // [2][L]
+  int *st_dst = st_exp + 2 * L;                // [2][L]
+  int *st_lst = st_dst + 2 * L;                // [2][CH]
+  {
+    const long long b = bslot(bv);
+    x += b * bv.x;
+    table += b * bv.t;
+    contrib += b * bv.c;
+  }
+  const long long nchunks = (count + CH - 1) / CH;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long ch, int s) {  // thread 0: stage chunk ch into buffer s
+    const long long m0 = ch * CH;
+    const int cnt = (int)min((long long)CH, count - m0);
+    const uint32_t sb = (uint32_t)(((long long)cnt * K * 4 + 15) & ~15LL);
+    const uint32_t lb = (uint32_t)((cnt * 4 + 15) & ~15);
+    const long long ebeg = e0 + m0 * K;
+    mbar_expect_tx(&bar[s], 3 * sb + lb);
+    bulk_g2s(st_var + s * L, var + ebeg, sb, &bar[s]);
+    bulk_g2s(st_exp + s * L, exps + ebeg, sb, &bar[s]);
+    bulk_g2s(st_dst + s * L, dst + ebeg, sb, &bar[s]);
+    bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
+  };
+  long long ch = blockIdx.x;
+  if (ch < nchunks && tid == 0) issue(ch, 0);
+  uint32_t phase[2] = {0, 0};
+  for (int s = 0; ch < nchunks; ch += gridDim.x, s ^= 1) {
+    const long long nxt = ch + gridDim.x;
+    if (nxt < nchunks && tid == 0) issue(nxt, s ^ 1);  // buffer s^1 was released by the last barrier
+    mbar_wait(&bar[s], phase[s]);
+    phase[s] ^= 1;
+    const long long m0 = ch * CH;
+    const int u = tid / G, r = tid % G;
+    const bool active = m0 + u < count;
+    const int uu = active ? u : 0;
+    const int *mv = st_var + s * L + uu * K;
+    const int *me = st_exp + s * L + uu * K;
+    const int *md = st_dst + s * L + uu * K;
+    const int c = st_lst[s * CH + uu];
+    const E co = eload<E>(coeff + (long long)c * es);
+    mono_tree_eval<E, BASE, G>(
+        r, active, K, mv, me, co, x, table, toff, [&](const E &v) { estore(contrib + (long long)c * es, v); },
+        [&](int t, const E &v) { estore(contrib + (long long)md[t] * es, v); });
+    __syncthreads();  // buffer s is free for the chunk after next
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1, k > 32: one CTA per monomial, tree levels in shared memory
 
 template <class E, int NT>
@@ -600,6 +676,27 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
                         double *contrib, int nb, const BView &bv, cudaStream_t st) {
   constexpr int G = TreeG<E>::value < BASE ? TreeG<E>::value : BASE;
   constexpr int NT = 128;
+  // dd/qd (compute-bound trees): 4 % faster on the cqd step; plain double is
+  // memory-bound and faster with one CTA per chunk (measured, profiles/r01)
+  const char *tv = getenv("PN_TREE_TMA");
+  const bool tma = tv ? strcmp(tv, "0") != 0 : Traits<E>::nc >= 2;
+  if (b.dense_k && tma) {
+    constexpr int CH = NT / G;
+    const size_t smem = (size_t)(6 * CH * b.dense_k + 2 * CH) * sizeof(int);
+    auto kern = k_mono_tree_tma<E, BASE, G, NT>;
+    if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+    const long long nchunks = (b.count + CH - 1) / CH;
+    // one resident wave of persistent CTAs (per slot share when batched)
+    const long long want = std::max(1LL, (long long)std::max(per_sm, 1) * num_sms() / std::max(nb, 1));
+    const dim3 grid((unsigned)std::min(nchunks, want), (unsigned)nb);
+    kern<<<grid, NT, smem, st>>>(b.d_list, b.count, b.dense_k, b.e0, sys->d_var, sys->d_exp, sys->d_dst, sys->d_coeff,
+                                 x, table, sys->d_toff, contrib, bv);
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+    return;
+  }
   const long long threads = b.count * G;
   const dim3 grid((unsigned)((threads + NT - 1) / NT), (unsigned)nb);
   k_mono_tree<E, BASE, G, NT><<<grid, NT, 0, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var, sys->d_exp,

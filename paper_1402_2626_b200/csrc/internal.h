@@ -161,6 +161,11 @@ struct pn_system {
     int base;
     long long count;
     int32_t *d_list;
+    // dense uniform bucket: every monomial has k = dense_k and the bucket's
+    // support entries are the contiguous block [e0, e0 + count*dense_k)
+    // (lets k_mono_tree_tma stage whole chunks with bulk copies); 0 if not
+    int dense_k = 0;
+    long long e0 = 0;
   };
   std::vector<Bucket> buckets;
 

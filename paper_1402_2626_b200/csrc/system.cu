@@ -44,7 +44,8 @@ namespace {
 template <class T>
 T *upload(const std::vector<T> &v) {
   T *p = nullptr;
-  size_t bytes = std::max<size_t>(v.size(), 1) * sizeof(T);
+  // +16 bytes: bulk copies of a last partial chunk round their size up to 16
+  size_t bytes = std::max<size_t>(v.size(), 1) * sizeof(T) + 16;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -311,6 +312,17 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
     bk.base = b >= 1 && b <= 5 ? (1 << b) : 0;
     bk.count = (long long)lists[b].size();
     bk.d_list = upload(lists[b]);
+    if (bk.kind == 1) {
+      const auto &L = lists[b];
+      const int K = cptr[L[0] + 1] - cptr[L[0]];
+      bool dense = cptr[L[0]] % 4 == 0;
+      for (size_t i = 0; dense && i < L.size(); ++i)
+        dense = cptr[L[i] + 1] - cptr[L[i]] == K && (int64_t)cptr[L[i]] == (int64_t)cptr[L[0]] + (int64_t)i * K;
+      if (dense) {
+        bk.dense_k = K;
+        bk.e0 = cptr[L[0]];
+      }
+    }
     S.buckets.push_back(bk);
   }
 
