@@ -1,6 +1,7 @@
 // newton.cu -- one Gauss-Newton correction, device resident end to end
 // (newton.py:82-103): f, J at x -> [J | -f] -> MGS least squares -> x + dx,
 // plus the field moduli the host turns into the reference's float norms.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -351,10 +352,46 @@ extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, cons
   const int W = B ? batch_width(sys, B) : 0;
   BatchSlots s;
   if (W) batch_alloc(sys, s, W, st);
+  // Slot groups on their own streams: while the host retires and refills one
+  // group, the other groups' kernels run, and one group's evaluation (HBM
+  // and latency heavy) overlaps another's FP64-bound solve.
+  constexpr int MAXG = 4;
+  int NG = 4;  // C5 2048 starts: 3848 / 3984 / 4040 / 4051 start-iter/s for 1..4 groups
+  if (const char *v = getenv("PN_BATCH_GROUPS")) NG = std::max(1, std::min(MAXG, atoi(v)));
+  NG = std::max(1, std::min(NG, W));
+  int gsplit[MAXG + 1];
+  for (int g = 0; g <= NG; ++g) gsplit[g] = (int)((long long)W * g / NG);
+  cudaStream_t gs[MAXG] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ready_ev = nullptr;
+  struct StreamGuard {
+    cudaStream_t *s;
+    cudaEvent_t *e;
+    ~StreamGuard() {
+      for (int g = 0; g < MAXG; ++g)
+        if (s[g]) cudaStreamDestroy(s[g]);
+      if (*e) cudaEventDestroy(*e);
+    }
+  } guard{gs, &ready_ev};
+  PN_CHECK_CUDA(cudaEventCreateWithFlags(&ready_ev, cudaEventDisableTiming));
+  PN_CHECK_CUDA(cudaEventRecord(ready_ev, st));
+  for (int g = 0; g < NG; ++g) {
+    PN_CHECK_CUDA(cudaStreamCreateWithFlags(&gs[g], cudaStreamNonBlocking));
+    PN_CHECK_CUDA(cudaStreamWaitEvent(gs[g], ready_ev, 0));
+  }
   std::vector<int64_t> owner(W, -1);
-  std::vector<int32_t> it((size_t)B, 0), flags(W), list;
+  std::vector<int32_t> it((size_t)B, 0);
+  // pinned host buffers, so the per-group copies stay asynchronous
+  int32_t *hbuf = nullptr;
+  PN_CHECK_CUDA(cudaMallocHost(&hbuf, sizeof(int32_t) * (2 * (size_t)W + 2)));
+  struct HostGuard {
+    int32_t *p;
+    ~HostGuard() { cudaFreeHost(p); }
+  } hguard{hbuf};
+  int32_t *flags = hbuf, *hlist = hbuf + W + 1;
+  std::vector<int32_t> list[MAXG];
+  bool pending[MAXG] = {false, false, false, false};
   int64_t next = 0;
-  auto load = [&](int slot) {
+  auto load = [&](int slot, cudaStream_t sg) {
     if (next >= B) {
       owner[slot] = -1;
       return;
@@ -362,30 +399,16 @@ extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, cons
     const int64_t b = next++;
     owner[slot] = b;
     PN_CHECK_CUDA(cudaMemcpyAsync(s.x.d() + slot * s.xs, xa_all.d() + b * n * es, n * ebytes,
-                                  cudaMemcpyDeviceToDevice, st));
+                                  cudaMemcpyDeviceToDevice, sg));
     if (consts)
       PN_CHECK_CUDA(cudaMemcpyAsync(s.k.d() + slot * s.ks, ca_all.d() + b * m * es, m * ebytes,
-                                    cudaMemcpyDeviceToDevice, st));
+                                    cudaMemcpyDeviceToDevice, sg));
   };
-  for (int w = 0; w < W; ++w) load(w);
-  while (true) {
-    list.clear();
-    for (int w = 0; w < W; ++w)
-      if (owner[w] >= 0) list.push_back(w);
-    if (list.empty()) break;
-    const int nb = (int)list.size();
-    PN_CHECK_CUDA(cudaMemcpyAsync(s.list.p, list.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
-    const int32_t *sl = s.list.as<int32_t>();
-    const BView bv{sl, s.xs, s.ts, s.cs, s.as, 0};
-    dispatch_level(sys->nc, sys->cplx, [&]<class E>() {
-      evaldiff_batch_impl<E>(sys, nb, bv, s.x.d(), s.table.d(), s.contrib.d(), nullptr, s.A.d(), n,
-                             cpos_d.as<int32_t>(), consts ? s.k.d() : nullptr, s.ks, st);
-      solve_batch_impl<E>(nb, sl, m, n, s.A.d(), s.as, s.Q.d(), s.qs, s.R.d(), s.rs, s.x.d(), s.xs, s.dx.d(), tol,
-                          s.flags.as<int32_t>(), st);
-    });
-    PN_CHECK_CUDA(cudaMemcpyAsync(flags.data(), s.flags.p, sizeof(int32_t) * W, cudaMemcpyDeviceToHost, st));
-    PN_CHECK_CUDA(cudaStreamSynchronize(st));
-    for (int w : list) {
+  for (int g = 0; g < NG; ++g)
+    for (int w = gsplit[g]; w < gsplit[g + 1]; ++w) load(w, gs[g]);
+  // retire finished starts of group g (its stream is synchronised)
+  auto retire = [&](int g) {
+    for (int w : list[g]) {
       const int64_t b = owner[w];
       const int f = flags[w];
       ++it[b];
@@ -398,9 +421,43 @@ extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, cons
       iters[b] = it[b];
       status[b] = stat;
       PN_CHECK_CUDA(cudaMemcpyAsync(xa_all.d() + b * n * es, s.x.d() + w * s.xs, n * ebytes,
-                                    cudaMemcpyDeviceToDevice, st));
-      load(w);
+                                    cudaMemcpyDeviceToDevice, gs[g]));
+      load(w, gs[g]);
     }
+  };
+  while (true) {
+    bool any = false;
+    for (int g = 0; g < NG; ++g) {
+      if (pending[g]) {
+        PN_CHECK_CUDA(cudaStreamSynchronize(gs[g]));
+        pending[g] = false;
+        retire(g);
+      }
+      list[g].clear();
+      for (int w = gsplit[g]; w < gsplit[g + 1]; ++w)
+        if (owner[w] >= 0) list[g].push_back(w);
+      if (list[g].empty()) continue;
+      any = true;
+      const int nb = (int)list[g].size();
+      int32_t *sl = s.list.as<int32_t>() + gsplit[g];
+      std::copy(list[g].begin(), list[g].end(), hlist + gsplit[g]);
+      PN_CHECK_CUDA(cudaMemcpyAsync(sl, hlist + gsplit[g], sizeof(int32_t) * nb, cudaMemcpyHostToDevice, gs[g]));
+      const BView bv{sl, s.xs, s.ts, s.cs, s.as, 0};
+      dispatch_level(sys->nc, sys->cplx, [&]<class E>() {
+        evaldiff_batch_impl<E>(sys, nb, bv, s.x.d(), s.table.d(), s.contrib.d(), nullptr, s.A.d(), n,
+                               cpos_d.as<int32_t>(), consts ? s.k.d() : nullptr, s.ks, gs[g]);
+        solve_batch_impl<E>(nb, sl, m, n, s.A.d(), s.as, s.Q.d(), s.qs, s.R.d(), s.rs, s.x.d(), s.xs, s.dx.d(),
+                            tol, s.flags.as<int32_t>(), gs[g]);
+      });
+      PN_CHECK_CUDA(cudaMemcpyAsync(flags + gsplit[g], s.flags.as<int32_t>() + gsplit[g],
+                                    sizeof(int32_t) * (gsplit[g + 1] - gsplit[g]), cudaMemcpyDeviceToHost, gs[g]));
+      pending[g] = true;
+    }
+    if (!any) break;
+  }
+  for (int g = 0; g < NG; ++g) {
+    PN_CHECK_CUDA(cudaEventRecord(ready_ev, gs[g]));
+    PN_CHECK_CUDA(cudaStreamWaitEvent(st, ready_ev, 0));
   }
   DevOut xo(x_out, (size_t)B * n * es, st);
   if (B) aos_to_planes(es, B * n, xa_all.d(), xo.d, st);
