@@ -209,10 +209,21 @@ __device__ __forceinline__ void load_rows_cg(E (&v)[B], const double *__restrict
 }
 
 // publish pivot k: make this CTA's Q/R writes visible, then raise the flag
+// diagnostics (PN_MGS_TRACE=file): global-timer stamp of every published pivot
+__device__ unsigned long long *g_mgs_trace = nullptr;
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void publish(int *ready, int k) {
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) st_release(ready + k, 1);
+  if (threadIdx.x == 0) {
+    st_release(ready + k, 1);
+    if (g_mgs_trace) g_mgs_trace[k] = globaltimer();
+  }
 }
 
 // wait for pivot k; false on failure (breakdown elsewhere or watchdog)
@@ -443,7 +454,7 @@ template <int B> struct Depth { static constexpr int value = B <= 1 ? 1 : B <= 2
 template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
-                                                    MgsStatus *status, int *ready) {
+                                                    MgsStatus *status, int *ready, int kstop) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
@@ -578,13 +589,16 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
     if (tid == 0) orig[j] = nrm.c[0];
   }
 
+  // Columns c >= kstop only receive the sweeps k < kstop here and are
+  // written back to A; k_mgs_tail finishes them (pivots kstop..n).
   poll();
   int lo = 0;
   while (lo < nown) {
     const int c = cta + lo * G;
+    const int tgt = c < kstop ? c : kstop;
     if (fail) return;
     const int dlo = done[lo];
-    if (dlo < c && dlo >= known) {
+    if (dlo < tgt && dlo >= known) {
       // critical column blocked on pivot dlo: catch a lagging column up
       int pick = -1;
       for (int i = lo + 1; i < nown; ++i)
@@ -611,7 +625,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
     // serve the critical column with every published sweep
     make_resident(lo);
     int d = dlo;
-    while (d < c) {
+    while (d < tgt) {
       if (d >= known) {
         poll();
         if (fail) return;
@@ -621,7 +635,16 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
       ++d;
     }
     done[lo] = d;
-    if (d < c) continue;
+    if (d < tgt) continue;
+    if (c >= kstop) {  // hand the column to the tail kernel
+      __syncthreads();
+      double *g = A + (long long)c * m * es;
+      for (int r = tid; r < m; r += NT) estore(g + (long long)r * es, col.get(r));
+      __syncthreads();
+      res = -1;
+      ++lo;
+      continue;
+    }
     // pivot c (mgs.py:176-193); c == n is the residual norm z
     const Rl rkk = norm();
     if (c < n) {
@@ -649,6 +672,153 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
     }
     res = -1;  // column c is final; nothing to write back
     ++lo;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_mgs_tail: the last C sweeps of the quad-double factorisation.  There the
+// flow kernel is critical-path bound (one pivot per ~64 us while only C
+// columns remain, profiles/r01 trace), so every remaining column is split
+// over S CTAs by aligned row blocks of RQ = NT*B rows.  Each part reduces its
+// block (the lower levels of tree_sum's tree), the S partials are exchanged
+// through global memory with release/acquire flags and combined in the same
+// pairwise order (the top levels), so r_kj, the norms and therefore Q and R
+// stay bit-identical.  Pivot j is published when all S parts have stored
+// their rows of q_j (ready[j] counts to S).
+template <class E, int B, int NT>
+__global__ void __launch_bounds__(NT, 4) k_mgs_tail(double *__restrict__ A, int m, int n, const double *__restrict__ orig,
+                                                 double eps, double *__restrict__ Q, double *__restrict__ R,
+                                                 MgsStatus *status, int *ready, int kstop, int S,
+                                                 double *__restrict__ xch, int *__restrict__ xflag) {
+  using Rl = typename Traits<E>::R;
+  constexpr int es = Traits<E>::es;
+  constexpr int RQ = NT * B;
+  __shared__ E sme[NT / 32];
+  __shared__ Rl smr[NT / 32];
+  __shared__ E s_r;
+  __shared__ Rl s_n;
+  __shared__ int s_ok;
+  const int ci = blockIdx.x / S, part = blockIdx.x % S;
+  const int j = kstop + ci;
+  const int tid = threadIdx.x;
+  const int row0 = part * RQ + tid * B;
+  const int valid = m - row0 <= 0 ? 0 : (m - row0 >= B ? B : m - row0);
+  const int prow = m - part * RQ;  // rows of this part (may exceed RQ)
+  const int nparts = prow <= 0 ? 0 : ((prow >= RQ ? RQ : prow) + B - 1) / B;
+  const int sparts = (m + RQ - 1) / RQ;  // parts with rows
+  const long long ldR = n + 1;
+  const double *col = A + (long long)j * m * es;
+  E a[B];
+#pragma unroll
+  for (int q = 0; q < B; ++q) a[q] = q < valid ? eload<E>(col + (long long)(row0 + q) * es) : ezero<E>();
+  // exchange slot of column ci: [2 parity][S] elements (E units) + flags
+  E *xe = reinterpret_cast<E *>(xch) + (long long)ci * 2 * S;
+  int *xf = xflag + (long long)ci * 2 * S;
+  // publish this part's partial with tag, gather all S, combine in tree order
+  auto exchange = [&](auto v, int tag) {
+    using T = decltype(v);
+    T *slot = reinterpret_cast<T *>(xe + (tag & 1) * S);
+    if (tid == 0) {
+      slot[part] = v;
+      __threadfence();
+      st_release(xf + (tag & 1) * S + part, tag);
+      bool ok = true;
+      long long t0 = clock64();
+      for (int p = 0; p < sparts && ok; ++p)
+        while (ld_acquire(xf + (tag & 1) * S + p) != tag) {
+          if (ld_acquire(&status->code)) { ok = false; break; }
+          if (clock64() - t0 > (1ll << 36)) {
+            atomicExch(&status->code, PN_E_CUDA);
+            ok = false;
+            break;
+          }
+        }
+      T acc = v;
+      if (ok) {
+        T w[8];
+        for (int p = 0; p < sparts; ++p) w[p] = eload_cg<T>(reinterpret_cast<const double *>(slot + p));
+        for (int st = 1; st < sparts; st <<= 1)
+          for (int p = 0; p + st < sparts; p += 2 * st) w[p] = eadd(w[p], w[p + st]);
+        acc = w[0];
+      }
+      s_ok = ok;
+      return acc;
+    }
+    return v;
+  };
+  for (int k = kstop; k <= j && k <= n; ++k) {
+    if (k < j) {
+      // wait for pivot k (all S parts of its column stored q_k)
+      if (tid == 0) {
+        long long t0 = clock64();
+        int ok = 1;
+        while (ld_acquire(ready + k) < S) {
+          if (ld_acquire(&status->code)) { ok = 0; break; }
+          __nanosleep(32);
+          if (clock64() - t0 > (1ll << 36)) {
+            atomicExch(&status->code, PN_E_CUDA);
+            ok = 0;
+            break;
+          }
+        }
+        s_ok = ok;
+      }
+      __syncthreads();
+      if (!s_ok) return;
+      const double *qk = Q + (long long)k * m * es;
+      E qv[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) qv[q] = q < valid ? eload_cg<E>(qk + (long long)(row0 + q) * es) : ezero<E>();
+      E pr[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), a[q]);
+      const E part_sum = block_tree_reduce<E, NT>(local_tree<E, B>(pr, valid), nparts, sme);
+      const E r = exchange(part_sum, k + 1);
+      if (tid == 0) s_r = r;
+      __syncthreads();
+      if (!s_ok) return;
+      const E rk = s_r;
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (q < valid) a[q] = esub(a[q], emul(qv[q], rk));
+      if (part == 0 && tid == 0) estore(R + ((long long)j * ldR + k) * es, rk);
+      __syncthreads();  // s_r / s_ok reuse
+      continue;
+    }
+    // pivot j (mgs.py:176-193); j == n is the residual norm z
+    Rl a2[B];
+#pragma unroll
+    for (int q = 0; q < B; ++q) a2[q] = eabs2(a[q]);
+    const Rl part_n = block_tree_reduce<Rl, NT>(local_tree<Rl, B>(a2, valid), nparts, smr);
+    const Rl tot = exchange(part_n, j + 1 + (1 << 30));
+    if (tid == 0) s_n = tot;
+    __syncthreads();
+    if (!s_ok) return;
+    const Rl rkk = fsqrt(s_n);
+    if (j < n) {
+      const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), orig[j]);
+      if (rkk.c[0] <= thr) {
+        if (part == 0 && tid == 0) {
+          status->k = j;
+          status->rkk = rkk.c[0];
+          status->thr = thr;
+          __threadfence();
+          atomicExch(&status->code, PN_E_BREAKDOWN);
+        }
+        return;
+      }
+    }
+    if (part == 0 && tid == 0) estore(R + ((long long)j * ldR + j) * es, eembed(rkk, (E *)nullptr));
+    if (j < n) {
+      const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+      double *qc = Q + (long long)j * m * es;
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (q < valid) estore(qc + (long long)(row0 + q) * es, ediv_prepared(a[q], p));
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(ready + j, 1);
+    }
   }
 }
 
@@ -888,6 +1058,27 @@ static bool try_mgs_warp(int m, int n, double *A, double *Q, double *R_, MgsWork
   return true;
 }
 
+static void trace_begin(int n, unsigned long long **buf) {
+  *buf = nullptr;
+  if (!getenv("PN_MGS_TRACE")) return;
+  PN_CHECK_CUDA(cudaMalloc(buf, sizeof(unsigned long long) * (n + 2)));
+  PN_CHECK_CUDA(cudaMemset(*buf, 0, sizeof(unsigned long long) * (n + 2)));
+  PN_CHECK_CUDA(cudaMemcpyToSymbol(g_mgs_trace, buf, sizeof(*buf)));
+}
+static void trace_end(int n, unsigned long long *buf, cudaStream_t st) {
+  if (!buf) return;
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> h(n + 2);
+  PN_CHECK_CUDA(cudaMemcpy(h.data(), buf, sizeof(unsigned long long) * (n + 2), cudaMemcpyDeviceToHost));
+  unsigned long long *null = nullptr;
+  PN_CHECK_CUDA(cudaMemcpyToSymbol(g_mgs_trace, &null, sizeof(null)));
+  cudaFree(buf);
+  if (FILE *f = fopen(getenv("PN_MGS_TRACE"), "w")) {
+    for (int k = 0; k <= n; ++k) fprintf(f, "%d %llu\n", k, h[k]);
+    fclose(f);
+  }
+}
+
 template <class E, int B, int NT>
 static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
   MgsStatus *status = w.status.as<MgsStatus>();
@@ -900,12 +1091,37 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
   const int grid = std::min(per_sm * num_sms(), n + 1);
   if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
+  // row-split tail (quad double): the last C columns, S CTAs each
+  constexpr int TB = 2, TNT = 128, RQ = TB * TNT;
+  int kstop = n + 1, S = (m + RQ - 1) / RQ, C = 0;
+  const char *tv = getenv("PN_MGS_TAIL");
+  if (Traits<E>::nc == 4 && S >= 2 && S <= 8 && !(tv && strcmp(tv, "0") == 0)) {
+    int tper = 0;
+    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, TB, TNT>, TNT, 0));
+    C = std::min(n + 1, tper * num_sms() / S);
+    if (tv && atoi(tv) > 0) C = std::min(C, atoi(tv));
+    if (C >= 16) kstop = n + 1 - C;
+    else C = 0;
+  }
   w.ready.ensure((size_t)(n + 1) * sizeof(int));
   PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
   int *ready = w.ready.as<int>();
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop};
+  unsigned long long *tr = nullptr;
+  trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
   count_launch(1);
+  if (C > 0) {
+    constexpr int es = Traits<E>::es;
+    DevBuf xch((size_t)C * 2 * S * es * sizeof(double) + 16, st), xfl((size_t)C * 2 * S * sizeof(int) + 16, st);
+    PN_CHECK_CUDA(cudaMemsetAsync(xfl.p, 0, (size_t)C * 2 * S * sizeof(int), st));
+    double *xp = xch.d();
+    int *xf = xfl.as<int>();
+    void *targs[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &S, &xp, &xf};
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_mgs_tail<E, TB, TNT>, C * S, TNT, targs, 0, st));
+    count_launch(1);
+  }
+  trace_end(n, tr, st);
   return true;
 }
 
