@@ -1091,13 +1091,16 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
   const int grid = std::min(per_sm * num_sms(), n + 1);
   if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
-  // row-split tail (quad double): the last C columns, S CTAs each
-  constexpr int TB = 2, TNT = 128, RQ = TB * TNT;
-  int kstop = n + 1, S = (m + RQ - 1) / RQ, C = 0;
+  // row-split tail (quad double): the last C columns, S CTAs each; parts of
+  // RQ = 256 rows (PN_MGS_TAIL_RQ=512 for half as many parts, twice the columns)
   const char *tv = getenv("PN_MGS_TAIL");
+  const char *rv = getenv("PN_MGS_TAIL_RQ");
+  const int RQ = (rv && atoi(rv) == 512) ? 512 : 256;
+  int kstop = n + 1, S = (m + RQ - 1) / RQ, C = 0;
   if (Traits<E>::nc == 4 && S >= 2 && S <= 8 && !(tv && strcmp(tv, "0") == 0)) {
     int tper = 0;
-    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, TB, TNT>, TNT, 0));
+    if (RQ == 512) PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, 4, 128>, 128, 0));
+    else PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, 2, 128>, 128, 0));
     C = std::min(n + 1, tper * num_sms() / S);
     if (tv && atoi(tv) > 0) C = std::min(C, atoi(tv));
     if (C >= 16) kstop = n + 1 - C;
@@ -1118,7 +1121,8 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
     double *xp = xch.d();
     int *xf = xfl.as<int>();
     void *targs[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &S, &xp, &xf};
-    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_mgs_tail<E, TB, TNT>, C * S, TNT, targs, 0, st));
+    const void *tk = RQ == 512 ? (const void *)k_mgs_tail<E, 4, 128> : (const void *)k_mgs_tail<E, 2, 128>;
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, 128, targs, 0, st));
     count_launch(1);
   }
   trace_end(n, tr, st);
