@@ -75,24 +75,50 @@ __device__ __forceinline__ void rs_level(E (&v)[P], int t, int nparts) {
 }
 
 // P simultaneous tree_sums over the CTA's row blocks; thread t holds the
-// partial of its block for each column.  Results land in sout[0..P).
-// sred holds NT/32 * P elements.  Ends with a barrier.
+// partial of its block for each column.  Results land in sout[par*P + c].
+// sred holds 2 * NT/32 * P elements, sout 2 * P: the buffers alternate with
+// the CTA-uniform parity `par` (flipped here), so consecutive reductions
+// need no trailing barrier.  The tree over the warps' partials runs on warp
+// 0 with 32/P lanes per column (a local pairwise tree over each lane's warp
+// partials, then shuffle levels), not serially in one thread.
 template <class E, int P, int NT>
-__device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout) {
+__device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout, int &par) {
   constexpr int NW = NT / 32;
+  constexpr int LPC0 = 32 / P;
+  constexpr int LPC = LPC0 < NW ? LPC0 : NW;  // lanes per column
+  constexpr int WPL = NW / LPC;               // warp partials per lane
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  E *sr = sred + par * NW * P;
+  E *so = sout + par * P;
   rs_level<E, P, 0>(v, t, nparts);
-  if (lane < P) sred[w * P + rs_col<P>(lane)] = v[0];
+  if (lane < P) sr[w * P + rs_col<P>(lane)] = v[0];
   __syncthreads();
-  if (t < P) {
+  if (w == 0) {
     const int nw = (nparts + 31) / 32;
+    const int c = lane / LPC, jl = lane % LPC;
+    const int cc = c < P ? c : 0;
+    E x[WPL];
 #pragma unroll
-    for (int s = 1; s < NW; s <<= 1)
-      for (int wi = 0; wi + s < NW; wi += 2 * s)
-        if (wi + s < nw) sred[wi * P + t] = eadd(sred[wi * P + t], sred[(wi + s) * P + t]);
-    sout[t] = sred[t];
+    for (int i = 0; i < WPL; ++i) x[i] = sr[(jl * WPL + i) * P + cc];
+#pragma unroll
+    for (int s = 1; s < WPL; s <<= 1)
+#pragma unroll
+      for (int i = 0; i + s < WPL; i += 2 * s)
+        if (jl * WPL + i + s < nw) x[i] = eadd(x[i], x[i + s]);
+    E acc = x[0];
+#pragma unroll
+    for (int s2 = 1; s2 < LPC; s2 <<= 1) {
+      const E o = eshfl_xor(acc, s2);
+      const bool upper = (jl & s2) != 0;
+      const bool absorb = ((jl & ~(2 * s2 - 1)) + s2) * WPL < nw;
+      const E lhs = upper ? o : acc;
+      const E rhs = upper ? acc : o;
+      acc = absorb ? eadd(lhs, rhs) : lhs;
+    }
+    if (jl == 0 && c < P) so[c] = acc;
   }
   __syncthreads();
+  par ^= 1;
 }
 
 // float() of a field element (xprec.py:153-154, 261-262); quad double uses
@@ -169,8 +195,9 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) double smem[];
   double *pan = smem;                                              // P x es planes x MP
-  E *sred = reinterpret_cast<E *>(pan + (size_t)P * es * MP);      // NW * P
-  E *sres = sred + NW * P;                                         // P
+  E *sred = reinterpret_cast<E *>(pan + (size_t)P * es * MP);      // 2 x NW * P
+  E *sres = sred + 2 * NW * P;                                     // 2 x P
+  int par = 0;  // parity of the double-buffered reduction slots
   __shared__ double s_orig[P];
   __shared__ double s_max[NW];
   __shared__ int s_sing;
@@ -217,17 +244,17 @@ __global__ void __launch_bounds__(NT, MINB)
       for (int q = 0; q < B; ++q) pr[q] = emul(econj(qv[q]), pget(c, q));
       part[c] = local_tree<E, B>(pr, valid);
     }
-    multi_tree_reduce<E, P, NT>(part, nparts, sred, sres);
+    const E *res = sres + par * P;
+    multi_tree_reduce<E, P, NT>(part, nparts, sred, sres, par);
 #pragma unroll
     for (int c = 0; c < P; ++c) {
       if (c < c0 || c >= np) continue;
-      const E rk = sres[c];
+      const E rk = res[c];
 #pragma unroll
       for (int q = 0; q < B; ++q)
         if (q < valid) pput(c, q, esub(pget(c, q), emul(qv[q], rk)));
     }
-    if (t >= c0 && t < np) estore(R + ((long long)(j0 + t) * ldR + k) * es, sres[t]);
-    __syncthreads();  // sres is reused by the next reduction
+    if (t >= c0 && t < np) estore(R + ((long long)(j0 + t) * ldR + k) * es, res[t]);
   };
 
   for (int j0 = 0; j0 <= n; j0 += P) {
@@ -250,8 +277,9 @@ __global__ void __launch_bounds__(NT, MINB)
         part[c] = local_tree<Rl, B>(a2, valid);
       }
       Rl *rred = reinterpret_cast<Rl *>(sred), *rres = reinterpret_cast<Rl *>(sres);
-      multi_tree_reduce<Rl, P, NT>(part, nparts, rred, rres);
-      if (t < np) s_orig[t] = fsqrt(rres[t]).c[0];
+      const Rl *res = rres + par * P;
+      multi_tree_reduce<Rl, P, NT>(part, nparts, rred, rres, par);
+      if (t < np) s_orig[t] = fsqrt(res[t]).c[0];
       __syncthreads();
     }
     // ---- left-looking: sweeps of every earlier pivot, q prefetched one ahead
@@ -368,7 +396,7 @@ static void launch_solve(int nb, const int32_t *slots, int m, int n, double *A, 
   constexpr int es = Traits<E>::es;
   const size_t pan = (size_t)P * es * NT * B * sizeof(double);
   const size_t bsub = (size_t)n * (2 * es + Traits<E>::nc) * sizeof(double);
-  const size_t smem = std::max(pan, bsub) + (size_t)(NT / 32 + 1) * P * es * sizeof(double);
+  const size_t smem = std::max(pan, bsub) + (size_t)2 * (NT / 32 + 1) * P * es * sizeof(double);
   PN_REQUIRE(smem <= 227 * 1024, PN_E_ARG, "batched solve: n=%d needs %zu B of shared memory", n, smem);
   auto kern = k_solve_batch<E, B, P, NT, MINB>;
   PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
