@@ -15,7 +15,7 @@ timeout 900 python bench.py --converge --rows 1536 --max-iters 10 > $O/c4_over.j
 timeout 900 python bench.py --batch 2048 --dim 256 --terms 256 --base dd > $O/c5_2048.json 2>$O/c5_2048.err; cat $O/c5_2048.json
 B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $O/launches_cqd.csv $B > /dev/null 2>$O/launch.err
-for spec in "mgs:k_mgs_flow" "tree:k_mono_tree" "seg:k_segments" "bsub:k_backsub"; do
+for spec in "mgs:k_mgs_flow" "tree:k_mono_tree" "seg:k_segments" "bsub:k_backsub" "tail:k_mgs_tail"; do
   name=${spec%%:*}; kern=${spec#*:}
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kern -c 1 -o /tmp/prof_$name $B > /dev/null 2>$O/$name.err
   ncu -i /tmp/prof_$name.ncu-rep --page details --csv > $O/${name}_details.csv 2>>$O/$name.err
@@ -26,5 +26,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none -k regex:k_solve_batch -s 1 -c 1 -o /tmp/prof_solve $C5 > /dev/null 2>$O/solve.err
 ncu -i /tmp/prof_solve.ncu-rep --page details --csv > $O/solve_details.csv 2>>$O/solve.err
 ncu -i /tmp/prof_solve.ncu-rep --page raw --csv > $O/solve_raw.csv 2>>$O/solve.err
-python scripts/ncu_summary.py $O/launches_cqd.csv $O/launches_c5.csv $O/mgs_raw.csv $O/tree_raw.csv $O/seg_raw.csv $O/bsub_raw.csv $O/solve_raw.csv > $O/summary.txt 2>&1
+python scripts/ncu_summary.py $O/launches_cqd.csv $O/launches_c5.csv $O/mgs_raw.csv $O/tree_raw.csv $O/seg_raw.csv $O/bsub_raw.csv $O/tail_raw.csv $O/solve_raw.csv > $O/summary.txt 2>&1
 du -sh gpurun_out
