@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
 // stay bit-identical.  Pivot j is published when all S parts have stored
 // their rows of q_j (ready[j] counts to S).
 template <class E, int B, int NT>
-__global__ void __launch_bounds__(NT, 4) k_mgs_tail(double *__restrict__ A, int m, int n, const double *__restrict__ orig,
+__global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ A, int m, int n, const double *__restrict__ orig,
                                                  double eps, double *__restrict__ Q, double *__restrict__ R,
                                                  MgsStatus *status, int *ready, int kstop, int S,
                                                  double *__restrict__ xch, int *__restrict__ xflag) {
@@ -1096,14 +1096,19 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
   // row-split tail (quad double): the last C columns, S CTAs each; parts of
   // RQ = 256 rows (PN_MGS_TAIL_RQ=512 for half as many parts, twice the columns)
+  // variants: "a" = 128 threads x 2 rows (4 CTAs/SM), "b" = 64 threads x 4
+  // rows (8 CTAs/SM, twice the columns), "c" = 128 x 4 (512-row parts)
   const char *tv = getenv("PN_MGS_TAIL");
-  const char *rv = getenv("PN_MGS_TAIL_RQ");
-  const int RQ = (rv && atoi(rv) == 512) ? 512 : 256;
+  const char *vv = getenv("PN_MGS_TAIL_VARIANT");
+  const char var = vv && *vv ? vv[0] : 'a';
+  const void *tk = (const void *)k_mgs_tail<E, 2, 128>;
+  int tnt = 128, RQ = 256;
+  if (var == 'b') { tk = (const void *)k_mgs_tail<E, 4, 64>; tnt = 64; RQ = 256; }
+  if (var == 'c') { tk = (const void *)k_mgs_tail<E, 4, 128>; tnt = 128; RQ = 512; }
   int kstop = n + 1, S = (m + RQ - 1) / RQ, C = 0;
   if (Traits<E>::nc == 4 && S >= 2 && S <= 8 && !(tv && strcmp(tv, "0") == 0)) {
     int tper = 0;
-    if (RQ == 512) PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, 4, 128>, 128, 0));
-    else PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_mgs_tail<E, 2, 128>, 128, 0));
+    PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, tk, tnt, 0));
     C = std::min(n + 1, tper * num_sms() / S);
     if (tv && atoi(tv) > 0) C = std::min(C, atoi(tv));
     if (C >= 16) kstop = n + 1 - C;
@@ -1124,8 +1129,7 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
     double *xp = xch.d();
     int *xf = xfl.as<int>();
     void *targs[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &S, &xp, &xf};
-    const void *tk = RQ == 512 ? (const void *)k_mgs_tail<E, 4, 128> : (const void *)k_mgs_tail<E, 2, 128>;
-    PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, 128, targs, 0, st));
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, tnt, targs, 0, st));
     count_launch(1);
   }
   trace_end(n, tr, st);
