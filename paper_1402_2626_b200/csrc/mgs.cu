@@ -1095,7 +1095,7 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   const int grid = std::min(per_sm * num_sms(), n + 1);
   if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
   // row-split tail (quad double): the last C columns, S CTAs each; parts of
-  // RQ = 256 rows (PN_MGS_TAIL_RQ=512 for half as many parts, twice the columns)
+  // RQ = 256 rows by default (see the variants below)
   // variants: "a" = 128 threads x 2 rows (4 CTAs/SM), "b" = 64 threads x 4
   // rows (8 CTAs/SM, twice the columns), "c" = 128 x 4 (512-row parts)
   const char *tv = getenv("PN_MGS_TAIL");

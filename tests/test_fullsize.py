@@ -117,3 +117,23 @@ def test_headline_cqd_newton_step_full_size(gpu):
     assert same(res.f, f)
     assert same(res.dx, dx)
     assert same(res.x_next, xn)
+
+
+@pytest.mark.parametrize("m,n", [(1536, 64), (700, 300)])
+def test_cqd_tail_split_vs_oracle(gpu, m, n):
+    """Row-split tail of the quad-double MGS (k_mgs_tail): m = 1536 puts every
+    column in the tail (six 256-row parts); m = 700 splits the work between the
+    flow kernel and the tail with a ragged third part."""
+    from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
+    from paper_1402_2626_b200.varith import VecContext
+    L = oracle_level("cqd")
+    rng = np.random.default_rng(m + n)
+    aug = rng.uniform(-1, 1, L.cshape + (m, n + 1))
+    aug.reshape(L.es, -1)[[i for i in range(L.es) if i % L.nc != 0]] *= 1e-17
+    aug = np.ascontiguousarray(aug)
+    res = least_squares_solve(AugmentedMatrix(VecContext(level_from_name("cqd")), aug))
+    x, z, Q, R = oracle.least_squares(L, aug, nthreads=os.cpu_count() or 1)
+    assert same(res.factors.R, R)
+    assert same(res.factors.Q, Q)
+    assert same(res.x, x)
+    assert res.z == z
