@@ -100,6 +100,7 @@ __device__ __forceinline__ E block_tree_reduce(E v, int nparts, E *sm) {
         E o = eshfl_down(x, s);
         if ((lane & (2 * s - 1)) == 0 && lane + s < nw) x = eadd(x, o);
       }
+      __syncwarp();  // every lane has read sm[] before lane 0 overwrites sm[0]
       if (lane == 0) sm[0] = x;
     }
     __syncthreads();
