@@ -1168,7 +1168,10 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
       int *ready = w.ready.as<int>();
       const int grid = std::min(per_sm * sms, n + 1);
       void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+      unsigned long long *tr = nullptr;
+      trace_begin(n, &tr);
       PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_mgs_dataflow<E, B>, grid, kMgsThreads, args, 0, st));
+      trace_end(n, tr, st);
       count_launch(1);
       return;
     }
