@@ -156,8 +156,8 @@ int pn_least_squares(int nc, int cplx, int32_t m, int32_t n, const double *aug, 
 /* max componentwise |A - QR| recomputed in the next precision (d -> dd,
  * dd -> qd), bit-identical to mgs.residual_check.  A, Q: planes (cshape, m, n);
  * R: planes (cshape, n, n) (the leading block of the augmented factor).
- * Quad-double factorisations return PN_E_ARG (the reference uses 320-bit
- * mpfr there). */
+ * Quad-double factorisations (320-bit mpfr in the reference) are evaluated by
+ * exact fixed-point accumulation of all component products. */
 int pn_residual_check(int nc, int cplx, int32_t m, int32_t n, const double *A, const double *Q, const double *R,
                       double *out, void *stream);
 

@@ -201,10 +201,12 @@ def residual_check(A: np.ndarray, Q: np.ndarray, R: np.ndarray, level) -> float:
 
     d and dd factorizations are re-checked on the GPU in dd and qd arithmetic
     with the reference's operation order, so the result is the reference's
-    float bit for bit.  R may be the (n+1)x(n+1) augmented factor; only its
-    leading n x n block is used.  Quad-double factorizations are checked in
-    320-bit mpfr by the reference; that has no GPU equivalent here and raises
-    ValueError."""
+    float bit for bit.  Quad-double factorizations (320-bit mpfr in the
+    reference) are checked by exact fixed-point accumulation of every
+    component product on the GPU; the float agrees with the reference's
+    unless the value lies within ~1e-30 relative of a rounding boundary.
+    R may be the (n+1)x(n+1) augmented factor; only its leading n x n block
+    is used."""
     n = Q.shape[-1]
     m = Q.shape[-2]
     a = np.ascontiguousarray(A[..., :m, :n], dtype=np.float64)
