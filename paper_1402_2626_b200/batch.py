@@ -54,42 +54,34 @@ def evaluate_batch(prep: PreparedSystem, X: np.ndarray) -> np.ndarray:
 
 def _with_constant_terms(packed: PackedSystem):
     """Copy of the system in which every polynomial has a constant term (a
-    placeholder 1 where the base has none); returns it and, per polynomial,
-    the index of the base constant monomial or -1."""
+    placeholder 1 where the base has none, appended at the polynomial's end:
+    canonical order puts it first anyway); returns it and, per polynomial,
+    the index of the base constant monomial or -1.  Vectorised over the CSR."""
     level = packed.level
     m = packed.n_eqs
-    ks = np.diff(packed.mon_ptr)
+    pp = np.asarray(packed.poly_ptr, np.int64)
+    ks = np.diff(np.asarray(packed.mon_ptr, np.int64))
+    is_const = ks == 0
+    poly_of = np.repeat(np.arange(m), np.diff(pp))
+    nconst = np.bincount(poly_of[is_const], minlength=m) if m else np.zeros(0, np.int64)
+    if (nconst > 1).any():
+        raise ValueError("duplicate constant term")
     base_const = np.full(m, -1, dtype=np.int64)
-    poly_ptr, mon_ptr, cols = [0], [0], []
-    for i in range(m):
-        lo, hi = int(packed.poly_ptr[i]), int(packed.poly_ptr[i + 1])
-        consts = np.nonzero(ks[lo:hi] == 0)[0]
-        if len(consts) > 1:
-            raise ValueError("duplicate constant term")
-        for c in range(lo, hi):
-            mon_ptr.append(mon_ptr[-1] + int(ks[c]))
-            cols.append(c)
-        if len(consts):
-            base_const[i] = lo + int(consts[0])
-        else:
-            mon_ptr.append(mon_ptr[-1])
-            cols.append(-1)
-        poly_ptr.append(len(mon_ptr) - 1)
+    base_const[poly_of[is_const]] = np.nonzero(is_const)[0]
+    lacking = np.nonzero(nconst == 0)[0]
+    # insert one empty monomial at the end of every polynomial lacking a constant
+    new_ks = np.insert(ks, pp[lacking + 1], 0)
+    mon_ptr = np.concatenate(([0], np.cumsum(new_ks))).astype(np.int32)
+    added = np.zeros(m + 1, np.int64)
+    added[1:] = np.cumsum(nconst == 0)
+    poly_ptr = (pp + added).astype(np.int32)
     coef = packed.coeffs.reshape(level.es, -1)
-    newc = np.zeros((level.es, len(cols)))
-    for j, c in enumerate(cols):
-        if c >= 0:
-            newc[:, j] = coef[:, c]
-        else:
-            newc[0, j] = 1.0  # placeholder, replaced per start
-    sel = [c for c in cols if c >= 0]
-    var_idx = np.concatenate([packed.var_idx[packed.mon_ptr[c]:packed.mon_ptr[c + 1]] for c in sel]) if sel else \
-        np.zeros(0, np.int32)
-    exps = np.concatenate([packed.exps[packed.mon_ptr[c]:packed.mon_ptr[c + 1]] for c in sel]) if sel else \
-        np.zeros(0, np.int32)
-    out = PackedSystem(level, packed.n_vars, np.asarray(poly_ptr, np.int32), np.asarray(mon_ptr, np.int32),
-                       var_idx.astype(np.int32), exps.astype(np.int32),
-                       np.ascontiguousarray(newc.reshape(level.cshape + (len(cols),))))
+    placeholder = np.zeros((level.es, 1))
+    placeholder[0, 0] = 1.0  # replaced per start
+    newc = np.insert(coef, pp[lacking + 1], placeholder, axis=1) if len(lacking) else coef.copy()
+    out = PackedSystem(level, packed.n_vars, poly_ptr, mon_ptr, np.asarray(packed.var_idx, np.int32).copy(),
+                       np.asarray(packed.exps, np.int32).copy(),
+                       np.ascontiguousarray(newc.reshape(level.cshape + (newc.shape[1],))))
     return out, base_const
 
 

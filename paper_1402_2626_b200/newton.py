@@ -242,28 +242,22 @@ def homotopy_start_system(system, z, t):
             polys.append(terms)
         return PolySystem(system.n_vars, polys)
     # packed: rebuild CSR with the constant appended last in each polynomial
-    poly_ptr, mon_ptr, var_idx, exps, cols = [0], [0], [], [], []
+    # (vectorised: drop the old constants, insert the new ones at the ends)
+    pp = np.asarray(packed.poly_ptr, np.int64)
     coef = packed.coeffs.reshape(level.es, -1)
-    for i in range(m):
-        for c in range(packed.poly_ptr[i], packed.poly_ptr[i + 1]):
-            if ks[c] == 0:
-                continue
-            a, b = packed.mon_ptr[c], packed.mon_ptr[c + 1]
-            var_idx.append(packed.var_idx[a:b])
-            exps.append(packed.exps[a:b])
-            mon_ptr.append(mon_ptr[-1] + (b - a))
-            cols.append(c)
-        if keep_const[i]:
-            mon_ptr.append(mon_ptr[-1])
-            cols.append(-1 - i)
-        poly_ptr.append(len(mon_ptr) - 1)
-    newc = np.empty((level.es, len(cols)))
-    for j, c in enumerate(cols):
-        newc[:, j] = coef[:, c] if c >= 0 else flat_total[:, -1 - c]
-    return PackedSystem(level, packed.n_vars, np.asarray(poly_ptr, np.int32), np.asarray(mon_ptr, np.int32),
-                        np.concatenate(var_idx).astype(np.int32) if var_idx else np.zeros(0, np.int32),
-                        np.concatenate(exps).astype(np.int32) if exps else np.zeros(0, np.int32),
-                        np.ascontiguousarray(newc.reshape(level.cshape + (len(cols),))))
+    keep = ks != 0
+    poly_of = np.repeat(np.arange(m), np.diff(pp))
+    kept_per_poly = np.bincount(poly_of[keep], minlength=m)
+    ends = np.concatenate(([0], np.cumsum(kept_per_poly)))[1:]  # end of each poly among the kept monomials
+    add = np.nonzero(keep_const)[0]
+    new_ks = np.insert(ks[keep], ends[add], 0)
+    new_coef = np.insert(coef[:, keep], ends[add], flat_total[:, add], axis=1)
+    added = np.concatenate(([0], np.cumsum(keep_const.astype(np.int64))))
+    poly_ptr = np.concatenate(([0], np.cumsum(kept_per_poly))) + added
+    mon_ptr = np.concatenate(([0], np.cumsum(new_ks)))
+    return PackedSystem(level, packed.n_vars, poly_ptr.astype(np.int32), mon_ptr.astype(np.int32),
+                        np.asarray(packed.var_idx, np.int32).copy(), np.asarray(packed.exps, np.int32).copy(),
+                        np.ascontiguousarray(new_coef.reshape(level.cshape + (new_coef.shape[1],))))
 
 
 def convergence_ratio(trace: IterationTrace, floor: float = 0.0) -> list:

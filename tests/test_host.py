@@ -164,3 +164,43 @@ def test_golden_fixture_manifest():
     assert len(names) >= 40
     g = golden("newton_c1")
     assert int(g["n_vars"]) == 32 and g["poly_ptr"][-1] == 32 * 32
+
+
+def test_with_constant_terms_host_logic():
+    """batch._with_constant_terms: every polynomial gets exactly one constant
+    term (a placeholder 1 where it had none), the other monomials keep their
+    order, and base_const points at the original constants."""
+    from paper_1402_2626_b200.batch import _with_constant_terms
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    from paper_1402_2626_b200.xprec import precision_level
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        level = precision_level(["d", "dd", "qd"][trial % 3], trial % 2 == 0)
+        m, n = int(rng.integers(1, 8)), 6
+        pp, mp, vi, had = [0], [0], [], []
+        for _ in range(m):
+            terms = [sorted(rng.choice(n, int(rng.integers(1, 4)), replace=False).tolist())
+                     for _ in range(int(rng.integers(0, 6)))]
+            hasc = bool(rng.random() < 0.5)
+            if hasc:
+                terms.insert(int(rng.integers(0, len(terms) + 1)), [])
+            had.append(hasc)
+            for vs in terms:
+                vi += vs
+                mp.append(len(vi))
+            pp.append(len(mp) - 1)
+        M = len(mp) - 1
+        coeffs = rng.uniform(-1, 1, level.cshape + (M,))
+        p = PackedSystem(level, n, np.array(pp, np.int32), np.array(mp, np.int32), np.array(vi, np.int32),
+                         np.ones(len(vi), np.int32), coeffs)
+        q, base = _with_constant_terms(p)
+        ks_q = np.diff(q.mon_ptr)
+        for i in range(m):
+            lo, hi = q.poly_ptr[i], q.poly_ptr[i + 1]
+            assert int((ks_q[lo:hi] == 0).sum()) == 1
+            assert (base[i] >= 0) == had[i]
+            if had[i]:
+                assert np.diff(p.mon_ptr)[base[i]] == 0
+        assert np.array_equal(q.var_idx, p.var_idx)
+        kept = ks_q[ks_q > 0]
+        assert np.array_equal(kept, np.diff(p.mon_ptr)[np.diff(p.mon_ptr) > 0])
