@@ -179,6 +179,93 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   } while (!ok);
 }
 
+// ---------------------------------------------------------------------------
+// multi-column tree reductions (warp reduce-scatter), shared by the batched
+// solve and the pipelined MGS
+// column carried by `lane` after the reduce-scatter levels of a P-wide reduction
+template <int P> __device__ __forceinline__ int rs_col(int lane) {
+  int c = 0;
+#pragma unroll
+  for (int l = 0; (1 << l) < P; ++l) c += ((lane >> l) & 1) * (P >> (l + 1));
+  return c;
+}
+
+// level LV of the warp phase: lanes t and t^s combine the nodes t&~(2s-1)
+// and (t&~(2s-1))+s; the lower node is the left operand, a missing upper
+// node (index >= nparts) passes the lower one through
+template <class E, int P, int LV>
+__device__ __forceinline__ void rs_level(E (&v)[P], int t, int nparts) {
+  constexpr int s = 1 << LV;
+  constexpr int cnt = (P >> LV) > 0 ? (P >> LV) : 1;
+  const bool upper = (t & s) != 0;
+  const bool absorb = ((t & ~(2 * s - 1)) + s) < nparts;
+  if constexpr (cnt > 1) {
+    constexpr int h = cnt / 2;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const E mine = upper ? v[h + i] : v[i];
+      const E send = upper ? v[i] : v[h + i];
+      const E recv = eshfl_xor(send, s);
+      const E lhs = upper ? recv : mine;
+      const E rhs = upper ? mine : recv;
+      v[i] = absorb ? eadd(lhs, rhs) : lhs;
+    }
+  } else {
+    const E recv = eshfl_xor(v[0], s);
+    const E lhs = upper ? recv : v[0];
+    const E rhs = upper ? v[0] : recv;
+    v[0] = absorb ? eadd(lhs, rhs) : lhs;
+  }
+  if constexpr (LV < 4) rs_level<E, P, LV + 1>(v, t, nparts);
+}
+
+// P simultaneous tree_sums over the CTA's row blocks; thread t holds the
+// partial of its block for each column.  Results land in sout[par*P + c].
+// sred holds 2 * NT/32 * P elements, sout 2 * P: the buffers alternate with
+// the CTA-uniform parity `par` (flipped here), so consecutive reductions
+// need no trailing barrier.  The tree over the warps' partials runs on warp
+// 0 with 32/P lanes per column (a local pairwise tree over each lane's warp
+// partials, then shuffle levels), not serially in one thread.
+template <class E, int P, int NT>
+__device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout, int &par) {
+  constexpr int NW = NT / 32;
+  constexpr int LPC0 = 32 / P;
+  constexpr int LPC = LPC0 < NW ? LPC0 : NW;  // lanes per column
+  constexpr int WPL = NW / LPC;               // warp partials per lane
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  E *sr = sred + par * NW * P;
+  E *so = sout + par * P;
+  rs_level<E, P, 0>(v, t, nparts);
+  if (lane < P) sr[w * P + rs_col<P>(lane)] = v[0];
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (nparts + 31) / 32;
+    const int c = lane / LPC, jl = lane % LPC;
+    const int cc = c < P ? c : 0;
+    E x[WPL];
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) x[i] = sr[(jl * WPL + i) * P + cc];
+#pragma unroll
+    for (int s = 1; s < WPL; s <<= 1)
+#pragma unroll
+      for (int i = 0; i + s < WPL; i += 2 * s)
+        if (jl * WPL + i + s < nw) x[i] = eadd(x[i], x[i + s]);
+    E acc = x[0];
+#pragma unroll
+    for (int s2 = 1; s2 < LPC; s2 <<= 1) {
+      const E o = eshfl_xor(acc, s2);
+      const bool upper = (jl & s2) != 0;
+      const bool absorb = ((jl & ~(2 * s2 - 1)) + s2) * WPL < nw;
+      const E lhs = upper ? o : acc;
+      const E rhs = upper ? acc : o;
+      acc = absorb ? eadd(lhs, rhs) : lhs;
+    }
+    if (jl == 0 && c < P) so[c] = acc;
+  }
+  __syncthreads();
+  par ^= 1;
+}
+
 // sequential pairwise tree over a register array of B elements where only
 // the first `valid` are present (aligned block; right-pruned)
 template <class E, int B>

@@ -962,6 +962,171 @@ __global__ void __launch_bounds__(32) k_mgs_warp(double *__restrict__ A, int m, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_mgs_pipe: the dataflow schedule with TMA-pipelined operands (d, dd; m a
+// multiple of 256).  The dataflow kernel stalls on the L2 latency of every
+// column it streams (ncu: long_scoreboard is its top stall for cdd).  Here a
+// CTA knows the order of its (sweep, column) applies in advance, so the next
+// column is brought into a second shared-memory buffer by a cp.async.bulk
+// (TMA) while the current one computes, and q_k arrives the same way once per
+// sweep.  Thread t owns rows t, t+256, ... (one row of each 256-row block),
+// which keeps shared-memory reads conflict-free on the bulk-copied layout;
+// each block's dot product is a block tree, reduced for all blocks at once by
+// the warp reduce-scatter, and the block sums are combined pairwise (aligned
+// 256-row blocks: the top levels of tree_sum's tree).  Column updates are
+// written back to A (and a generic->async proxy fence orders them before the
+// later bulk copy of the same column).
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// block sums of NQ aligned 256-row blocks (reduce-scatter), then their
+// pairwise tree (absorb rule over the blocks)
+template <class T, int P, int NQ, int NT>
+__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par) {
+  const T *res = out + par * P;
+  multi_tree_reduce<T, P, NT>(v, NT, part, out, par);
+  T acc = res[0];
+  if constexpr (NQ == 2) acc = eadd(res[0], res[1]);
+  if constexpr (NQ == 3) acc = eadd(eadd(res[0], res[1]), res[2]);
+  if constexpr (NQ == 4) acc = eadd(eadd(res[0], res[1]), eadd(res[2], res[3]));
+  return acc;
+}
+
+template <class E, int NQ>
+__global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int m, int n, double *__restrict__ orig,
+                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
+                                                     MgsStatus *status, int *ready) {
+  using Rl = typename Traits<E>::R;
+  constexpr int NT = 256;
+  constexpr int es = Traits<E>::es;
+  constexpr int P = NQ == 1 ? 1 : (NQ == 2 ? 2 : 4);  // reduce-scatter width (power of two)
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(128) double pipe_smem[];
+  E *colb = reinterpret_cast<E *>(pipe_smem);  // [2][m]
+  E *qb = colb + 2 * m;                        // [m]
+  __shared__ E s_pe[2 * NW * P], s_oe[2 * P];
+  __shared__ Rl s_pr[2 * NW * P], s_or[2 * P];
+  __shared__ __align__(8) uint64_t bar[3];     // col0, col1, q
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const uint32_t cbytes = (uint32_t)m * es * sizeof(double);
+  int par = 0;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t ph[3] = {0, 0, 0};
+  auto col_norm = [&](const E (&a)[NQ]) -> Rl {
+    Rl v[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) v[q] = q < NQ ? eabs2(a[q]) : ezero<Rl>();
+    return fsqrt(pipe_block_sum<Rl, P, NQ, NT>(v, s_pr, s_or, par));
+  };
+  // initial column norms of the owned columns (mgs.py:171-172)
+  for (int j = cta; j < n; j += G) {
+    E a[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a[q] = eload<E>(A + ((long long)j * m + q * NT + tid) * es);
+    const Rl nrm = col_norm(a);
+    if (tid == 0) orig[j] = nrm.c[0];
+  }
+  __syncthreads();
+  auto pivot = [&](int c, const E (&a)[NQ]) -> bool {  // (mgs.py:176-193)
+    const Rl rkk = col_norm(a);
+    if (c < n) {
+      const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), orig[c]);
+      if (rkk.c[0] <= thr) {
+        if (tid == 0) {
+          status->k = c;
+          status->rkk = rkk.c[0];
+          status->thr = thr;
+          __threadfence();
+          atomicExch(&status->code, PN_E_BREAKDOWN);
+        }
+        publish(ready, c);
+        return false;
+      }
+    }
+    if (tid == 0) estore(R + ((long long)c * (n + 1) + c) * es, eembed(rkk, (E *)nullptr));
+    if (c < n) {
+      const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) estore(Q + ((long long)c * m + q * NT + tid) * es, ediv_prepared(a[q], p));
+      fence_proxy_async();
+      publish(ready, c);
+    }
+    return true;
+  };
+  if (cta == 0) {  // pivot 0
+    E a[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) a[q] = eload<E>(A + ((long long)q * NT + tid) * es);
+    if (!pivot(0, a)) return;
+  }
+  auto first_after = [&](int k) { return k + 1 + (((cta - (k + 1)) % G) + G) % G; };
+  auto issue_col = [&](int j, int b) {  // thread 0
+    fence_proxy_async();
+    mbar_expect_tx(&bar[b], cbytes);
+    bulk_g2s(colb + (size_t)b * m, A + (long long)j * m * es, cbytes, &bar[b]);
+  };
+  int s = 0;
+  int inbuf = -1;  // column whose current rows are in colb[s] (no copy pending)
+  if (tid == 0 && first_after(0) <= n) issue_col(first_after(0), 0);
+  for (int k = 0; k < n; ++k) {
+    const int j0 = first_after(k);
+    if (j0 > n) break;
+    if (!wait_pivot(ready, k, status)) return;
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[2], cbytes);
+      bulk_g2s(qb, Q + (long long)k * m * es, cbytes, &bar[2]);
+    }
+    mbar_wait(&bar[2], ph[2]);
+    ph[2] ^= 1;
+    for (int j = j0; j <= n; j += G) {
+      int jn = j + G;
+      if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
+      const bool pf = jn <= n && jn != j;
+      if (pf && tid == 0) issue_col(jn, s ^ 1);
+      if (inbuf != j) {
+        mbar_wait(&bar[s], ph[s]);
+        ph[s] ^= 1;
+      }
+      E a[NQ];
+      E *cb = colb + (size_t)s * m;
+      E v[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        if (q < NQ) {
+          a[q] = cb[q * NT + tid];
+          v[q] = emul(econj(qb[q * NT + tid]), a[q]);
+        } else {
+          v[q] = ezero<E>();
+        }
+      }
+      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par);
+      double *col = A + (long long)j * m * es;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        a[q] = esub(a[q], emul(qb[q * NT + tid], r));
+        cb[q * NT + tid] = a[q];
+        estore(col + ((long long)q * NT + tid) * es, a[q]);
+      }
+      fence_proxy_async();
+      if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
+      if (j == k + 1 && !pivot(k + 1, a)) return;
+      __syncthreads();  // colb[s] and the reduction slots are free
+      if (pf) {
+        s ^= 1;
+        inbuf = -1;
+      } else {
+        inbuf = (jn == j) ? j : -1;
+      }
+    }
+  }
+}
+
 // back substitution R x = y, y = R[:n, n] (mgs.py:229-247): descending j,
 // x_j = y_j / r_jj (full complex division), y[:j] -= R[:j, j] x_j.  The
 // division's reciprocal depends on r_jj only, so it is prepared for all j
@@ -1037,7 +1202,8 @@ static int mgs_mode(int nc) {
   if (v && strcmp(v, "dataflow") == 0) return 1;
   if (v && strcmp(v, "flow") == 0) return 0;
   if (v && strcmp(v, "warp") == 0) return 3;
-  return nc == 4 ? 0 : 1;
+  if (v && strcmp(v, "pipe") == 0) return 4;
+  return nc == 4 ? 0 : 4;
 }
 
 // warp-per-column schedule when every column owner fits on the GPU at once
@@ -1136,6 +1302,30 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   return true;
 }
 
+template <class E, int NQ>
+static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
+  MgsStatus *status = w.status.as<MgsStatus>();
+  double *orig = w.orig.d();
+  const double eps = level_eps(Traits<E>::nc);
+  const size_t smem = (size_t)3 * m * Traits<E>::es * sizeof(double);
+  auto kern = k_mgs_pipe<E, NQ>;
+  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  if (per_sm <= 0) return false;
+  const int grid = std::min(per_sm * num_sms(), n + 1);
+  w.ready.ensure((size_t)(n + 1) * sizeof(int));
+  PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+  int *ready = w.ready.as<int>();
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+  unsigned long long *tr = nullptr;
+  trace_begin(n, &tr);
+  PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, 256, args, smem, st));
+  trace_end(n, tr, st);
+  count_launch(1);
+  return true;
+}
+
 template <class E, int B>
 static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
   MgsStatus *status = w.status.as<MgsStatus>();
@@ -1151,6 +1341,16 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     else done = try_mgs_warp<E, 32>(m, n, A, Q, R, w, st);
     if (done) return;
   }
+  if (mode == 4 && Traits<E>::nc <= 2 && m % 256 == 0 && m <= 1024) {
+    bool done = false;
+    switch (m / 256) {
+      case 1: done = pipe_launch<E, 1>(m, n, A, Q, R, w, st); break;
+      case 2: done = pipe_launch<E, 2>(m, n, A, Q, R, w, st); break;
+      case 3: done = pipe_launch<E, 3>(m, n, A, Q, R, w, st); break;
+      default: done = pipe_launch<E, 4>(m, n, A, Q, R, w, st); break;
+    }
+    if (done) return;
+  }
   if (mode == 0) {
     // 6 warps x 8 rows for 1024 < m <= 1536 (the C4 overdetermined shape):
     // a 96 KB column, two CTAs per SM instead of one 128 KB CTA
@@ -1159,7 +1359,7 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
-  if (mode <= 1) {
+  if (mode <= 1 || mode == 4) {
     int per_sm = 0;
     PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_dataflow<E, B>, kMgsThreads, 0));
     if (per_sm > 0) {

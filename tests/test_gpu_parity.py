@@ -186,7 +186,7 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp", "pipe"])
 def mgs_mode(request, monkeypatch):
     """Every MGS schedule (priority flow, dataflow, launch per sweep, warp per column)."""
     monkeypatch.setenv("PN_MGS_MODE", request.param)
@@ -219,7 +219,8 @@ def test_breakdown_golden(gpu, mgs_mode):
     assert (e.value.k, e.value.rkk, e.value.threshold) == (int(k), rkk, thr)
 
 
-@pytest.mark.parametrize("lv,m,n", [("cqd", 160, 128), ("cdd", 513, 200), ("rdd", 1030, 64), ("cd", 256, 256)])
+@pytest.mark.parametrize("lv,m,n", [("cqd", 160, 128), ("cdd", 513, 200), ("rdd", 1030, 64), ("cd", 256, 256),
+                                    ("cdd", 768, 300), ("rd", 512, 512), ("cdd", 1024, 160)])
 def test_least_squares_vs_oracle(gpu, mgs_mode, lv, m, n):
     from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
     from paper_1402_2626_b200.varith import VecContext
@@ -236,15 +237,15 @@ def test_least_squares_vs_oracle(gpu, mgs_mode, lv, m, n):
     assert res.z == z
 
 
-@pytest.mark.parametrize("lv", ["cdd", "rqd", "cd"])
-def test_breakdown_mid_factorisation_vs_oracle(gpu, mgs_mode, lv):
+@pytest.mark.parametrize("lv,m", [("cdd", 300), ("rqd", 300), ("cd", 300), ("cdd", 512), ("rd", 512)])
+def test_breakdown_mid_factorisation_vs_oracle(gpu, mgs_mode, lv, m):
     """A dependent column deep in the matrix: every CTA of the dataflow kernel
     must stop cleanly and report the reference's (k, rkk, threshold)."""
     from paper_1402_2626_b200.mgs import AugmentedMatrix, MgsBreakdownError, mgs_qr
     from paper_1402_2626_b200.varith import VecContext
     L = oracle_level(lv)
     rng = np.random.default_rng(17)
-    aug = rng.uniform(-1, 1, L.cshape + (300, 201))
+    aug = rng.uniform(-1, 1, L.cshape + (m, 201))
     aug[..., 157] = aug[..., 3] * 0.5  # exact multiple of column 3
     aug = np.ascontiguousarray(aug)
     with pytest.raises(oracle.Breakdown) as want:
