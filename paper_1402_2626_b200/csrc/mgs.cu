@@ -1514,54 +1514,59 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict
 // the rest of the grid updates all rows above that, one lane per row, with
 // one grid barrier per block (as k_backsub_blocked).
 
-__device__ __forceinline__ F<4> shfl_f4(const F<4> &v, int src) {
-  F<4> r;
+template <int NC>
+__device__ __forceinline__ F<NC> shfl_fn(const F<NC> &v, int src) {
+  F<NC> r;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) r.c[i] = __shfl_sync(0xffffffffu, v.c[i], src);
+  for (int i = 0; i < NC; ++i) r.c[i] = __shfl_sync(0xffffffffu, v.c[i], src);
   return r;
 }
-__device__ __forceinline__ F<4> shfl_xor_f4(const F<4> &v, int mask) {
-  F<4> r;
+template <int NC>
+__device__ __forceinline__ F<NC> shfl_xor_fn(const F<NC> &v, int mask) {
+  F<NC> r;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) r.c[i] = __shfl_xor_sync(0xffffffffu, v.c[i], mask);
+  for (int i = 0; i < NC; ++i) r.c[i] = __shfl_xor_sync(0xffffffffu, v.c[i], mask);
   return r;
 }
 // a*b on a group of four lanes (p = lane & 3): p0 ar*br, p1 ai*bi, p2 ar*bi,
 // p3 ai*br; re = t1 - t2 on p0, im = t3 + t4 on p2.  Every lane of the warp
 // must call it (full-mask shuffles); all four lanes get the result.
-__device__ __forceinline__ C<4> lp_cmul(const C<4> &a, const C<4> &b, int p, int g4) {
-  const F<4> x = (p == 0 || p == 2) ? a.re : a.im;
-  const F<4> y = (p == 0 || p == 3) ? b.re : b.im;
-  const F<4> prod = qd_mul_call(x, y);
-  const F<4> other = shfl_xor_f4(prod, 1);
-  const F<4> v = qd_add_call(prod, p == 0 ? fneg(other) : other);
-  return {shfl_f4(v, g4), shfl_f4(v, g4 + 2)};
+template <int NC>
+__device__ __forceinline__ C<NC> lp_cmul(const C<NC> &a, const C<NC> &b, int p, int g4) {
+  const F<NC> x = (p == 0 || p == 2) ? a.re : a.im;
+  const F<NC> y = (p == 0 || p == 3) ? b.re : b.im;
+  const F<NC> prod = fmul(x, y);
+  const F<NC> other = shfl_xor_fn(prod, 1);
+  const F<NC> v = fadd(prod, p == 0 ? fneg(other) : other);
+  return {shfl_fn(v, g4), shfl_fn(v, g4 + 2)};
 }
 // a - b: p0 re, p1 im
-__device__ __forceinline__ C<4> lp_csub(const C<4> &a, const C<4> &b, int p, int g4) {
-  const F<4> v = qd_add_call((p & 1) ? a.im : a.re, fneg((p & 1) ? b.im : b.re));
-  return {shfl_f4(v, g4), shfl_f4(v, g4 + 1)};
+template <int NC>
+__device__ __forceinline__ C<NC> lp_csub(const C<NC> &a, const C<NC> &b, int p, int g4) {
+  const F<NC> v = fadd((p & 1) ? a.im : a.re, fneg((p & 1) ? b.im : b.re));
+  return {shfl_fn(v, g4), shfl_fn(v, g4 + 1)};
 }
 // y / r as (y * conj r) * recip(|r|^2) (varith.py:130-136 with the hoisted reciprocal)
-__device__ __forceinline__ C<4> lp_div(const C<4> &yv, const C<4> &r, const RDiv<4> &pr, int p, int g4) {
-  const C<4> num = lp_cmul(yv, cconj(r), p, g4);
-  const F<4> v = qd_mul_call((p & 1) ? num.im : num.re, pr.v);
-  return {shfl_f4(v, g4), shfl_f4(v, g4 + 1)};
+template <int NC>
+__device__ __forceinline__ C<NC> lp_div(const C<NC> &yv, const C<NC> &r, const RDiv<NC> &pr, int p, int g4) {
+  const C<NC> num = lp_cmul(yv, cconj(r), p, g4);
+  const F<NC> v = rdiv_apply((p & 1) ? num.im : num.re, pr);
+  return {shfl_fn(v, g4), shfl_fn(v, g4 + 1)};
 }
 
-template <int NT>
+template <int NC, int NT>
 __global__ void __launch_bounds__(NT) k_backsub_lanes(const double *__restrict__ R, int n, double *__restrict__ x,
-                                                      RDiv<4> *__restrict__ prep, double *__restrict__ y,
+                                                      RDiv<NC> *__restrict__ prep, double *__restrict__ y,
                                                       int *sing, MgsStatus *status) {
   namespace cg = cooperative_groups;
-  using E = C<4>;
-  constexpr int es = 8;
+  using E = C<NC>;
+  constexpr int es = 2 * NC;
   static_assert(NT == 128, "CTA 0 is 32 rows x 4 lanes");
   extern __shared__ __align__(16) double bl_smem[];
   E *sD = reinterpret_cast<E *>(bl_smem);  // 32 x 32 diagonal block, column-major
   E *sU = sD + 32 * 32;                     // 32 x 32 block above it
   E *sX = sU + 32 * 32;                     // x of the current block
-  RDiv<4> *sP = reinterpret_cast<RDiv<4> *>(sX + 32);
+  RDiv<NC> *sP = reinterpret_cast<RDiv<NC> *>(sX + 32);
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;
   const long long ld = n + 1;
@@ -1643,7 +1648,10 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
   constexpr int es = Traits<E>::es;
   DevBuf prep((size_t)n * Traits<E>::nc * sizeof(double) + 16, st);
   const char *mode = getenv("PN_BACKSUB_MODE");
-  if constexpr (std::is_same_v<E, C<4>>) {
+  // complex qd: four lanes per row (default).  Complex dd measured slower
+  // with lanes (1.18 vs 1.0 ms at n = 1024): its chain is short already.
+  if constexpr (Traits<E>::cplx && Traits<E>::nc == 4) {
+    constexpr int NC = Traits<E>::nc;
     if (!(mode && (strcmp(mode, "single") == 0 || strcmp(mode, "blocked") == 0))) {
       constexpr int NT = 128;
       DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
@@ -1651,14 +1659,14 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
       int *sing = sbuf.as<int>();
       PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
       const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
-      RDiv<4> *pp = prep.as<RDiv<4>>();
+      RDiv<NC> *pp = prep.as<RDiv<NC>>();
       double *yp = yw.d();
       MgsStatus *status = w.status.as<MgsStatus>();
       void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
-      const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<4>);
-      PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_lanes<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<NC>);
+      PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_lanes<NC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
-      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_lanes<NT>, grid, NT, args, smem, st));
+      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_lanes<NC, NT>, grid, NT, args, smem, st));
       count_launch(1);
       return;
     }
