@@ -980,10 +980,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // block sums of NQ aligned 256-row blocks (reduce-scatter), then their
 // pairwise tree (absorb rule over the blocks)
-template <class T, int P, int NQ, int NT, class Hook = NoHook>
-__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par, Hook &&hook = Hook{}) {
+template <class T, int P, int NQ, int NT>
+__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par) {
   const T *res = out + par * P;
-  multi_tree_reduce<T, P, NT>(v, NT, part, out, par, hook);
+  multi_tree_reduce<T, P, NT>(v, NT, part, out, par);
   T acc = res[0];
   if constexpr (NQ == 2) acc = eadd(res[0], res[1]);
   if constexpr (NQ == 3) acc = eadd(eadd(res[0], res[1]), res[2]);
@@ -1088,6 +1088,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       int jn = j + G;
       if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
       const bool pf = jn <= n && jn != j;
+      if (pf && tid == 0) issue_col(jn, s ^ 1);
       if (inbuf != j) {
         mbar_wait(&bar[s], ph[s]);
         ph[s] ^= 1;
@@ -1104,11 +1105,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
           v[q] = ezero<E>();
         }
       }
-      // the prefetch of the next column into the other buffer is issued once
-      // every thread is past the previous apply (first barrier of this one)
-      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par, [&]() {
-        if (pf) issue_col(jn, s ^ 1);
-      });
+      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par);
       double *col = A + (long long)j * m * es;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -1119,6 +1116,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       fence_proxy_async();
       if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
       if (j == k + 1 && !pivot(k + 1, a)) return;
+      __syncthreads();  // colb[s] and the reduction slots are free
       if (pf) {
         s ^= 1;
         inbuf = -1;
