@@ -991,7 +991,7 @@ __device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par
   return acc;
 }
 
-template <class E, int NQ>
+template <class E, int NQ, int QB>
 __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                      double eps, double *__restrict__ Q, double *__restrict__ R,
                                                      MgsStatus *status, int *ready) {
@@ -1002,10 +1002,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   constexpr int NW = NT / 32;
   extern __shared__ __align__(128) double pipe_smem[];
   E *colb = reinterpret_cast<E *>(pipe_smem);  // [2][m]
-  E *qb = colb + 2 * m;                        // [m]
+  E *qbuf = colb + 2 * m;                      // [QB][m] (QB = 2: q_{k+1} prefetched)
   __shared__ E s_pe[2 * NW * P], s_oe[2 * P];
   __shared__ Rl s_pr[2 * NW * P], s_or[2 * P];
-  __shared__ __align__(8) uint64_t bar[3];     // col0, col1, q
+  __shared__ __align__(8) uint64_t bar[4];     // col0, col1, q0, q1
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const uint32_t cbytes = (uint32_t)m * es * sizeof(double);
   int par = 0;
@@ -1013,10 +1013,11 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
+    mbar_init(&bar[3], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t ph[3] = {0, 0, 0};
+  uint32_t ph[4] = {0, 0, 0, 0};
   auto col_norm = [&](const E (&a)[NQ]) -> Rl {
     Rl v[P];
 #pragma unroll
@@ -1072,23 +1073,35 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   };
   int s = 0;
   int inbuf = -1;  // column whose current rows are in colb[s] (no copy pending)
+  int qs = 0;      // q buffer of the current sweep
+  int qpre = -1;   // (thread 0) sweep whose q is already being copied into the other buffer
+  auto issue_q = [&](int k, int b) {  // thread 0
+    fence_proxy_async();
+    mbar_expect_tx(&bar[2 + b], cbytes);
+    bulk_g2s(qbuf + (size_t)b * m, Q + (long long)k * m * es, cbytes, &bar[2 + b]);
+  };
   if (tid == 0 && first_after(0) <= n) issue_col(first_after(0), 0);
   for (int k = 0; k < n; ++k) {
     const int j0 = first_after(k);
     if (j0 > n) break;
     if (!wait_pivot(ready, k, status)) return;
-    if (tid == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&bar[2], cbytes);
-      bulk_g2s(qb, Q + (long long)k * m * es, cbytes, &bar[2]);
-    }
-    mbar_wait(&bar[2], ph[2]);
-    ph[2] ^= 1;
+    if (QB == 2) qs = k & 1;
+    if (tid == 0 && qpre != k) issue_q(k, qs);
+    mbar_wait(&bar[2 + qs], ph[2 + qs]);
+    ph[2 + qs] ^= 1;
+    const E *qb = qbuf + (size_t)qs * m;
     for (int j = j0; j <= n; j += G) {
       int jn = j + G;
       if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
       const bool pf = jn <= n && jn != j;
       if (pf && tid == 0) issue_col(jn, s ^ 1);
+      // q_{k+1} into the other buffer as soon as it is published (its last
+      // reader, sweep k-1, finished before this sweep's first barrier)
+      if (QB == 2 && tid == 0 && qpre != k + 1 && k + 1 < n && first_after(k + 1) <= n &&
+          ld_acquire(ready + k + 1)) {
+        issue_q(k + 1, qs ^ 1);
+        qpre = k + 1;
+      }
       if (inbuf != j) {
         mbar_wait(&bar[s], ph[s]);
         ph[s] ^= 1;
@@ -1307,8 +1320,11 @@ static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   MgsStatus *status = w.status.as<MgsStatus>();
   double *orig = w.orig.d();
   const double eps = level_eps(Traits<E>::nc);
-  const size_t smem = (size_t)3 * m * Traits<E>::es * sizeof(double);
-  auto kern = k_mgs_pipe<E, NQ>;
+  // QB = 2 (q_{k+1} prefetched as soon as it is published) measured slower
+  // for cd (5.3 -> 5.7 ms: thread 0's per-apply flag poll delays every apply)
+  constexpr int QB = 1;
+  const size_t smem = (size_t)(2 + QB) * m * Traits<E>::es * sizeof(double);
+  auto kern = k_mgs_pipe<E, NQ, QB>;
   PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
