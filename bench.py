@@ -346,7 +346,9 @@ def run_ours(args):
     t_fac = statistics.median(p[3] for p in phases)
     mgs_rate = w_factor / t_fac
     workload = f"F({args.dim},{args.terms},{args.k}) complex {args.base} {m}x{n}"
-    mgs_kernel = "k_mgs_flow" if nc == 4 else "k_mgs_dataflow"
+    # the schedule mgs.cu's mgs_mode picks by default for this shape
+    mgs_kernel = ("k_mgs_flow" if nc == 4 else
+                  "k_mgs_pipe" if m % 256 == 0 and m <= 1024 else "k_mgs_dataflow")
     roofline = {"bound": "fp64", "kernel": f"{mgs_kernel} (MGS factorisation of [J | -f], one launch per step)",
                 "achieved": mgs_rate / 1e12, "peak": fp64_peak / 1e12, "unit": "T FP64-instr/s",
                 "frac": mgs_rate / fp64_peak, "traffic": committed_traffic(mgs_kernel, workload),

@@ -1206,9 +1206,11 @@ static double level_eps(int nc) { return nc == 1 ? 0x1p-53 : nc == 2 ? 0x1p-104 
 
 // PN_MGS_MODE=sweeps selects the launch-per-sweep schedule (kept as the
 // reference schedule for tests); the default is the persistent dataflow kernel.
-// 0 flow, 1 dataflow, 2 sweeps.  Default by measurement (profiles/r01): the
-// priority/smem schedule wins when sweeps are compute-heavy (quad double);
-// the plain dataflow kernel has the shorter per-sweep latency for d/dd.
+// 0 flow, 1 dataflow, 2 sweeps, 3 warp, 4 pipe.  Default by measurement
+// (profiles/r01): the priority/smem schedule wins when sweeps are
+// compute-heavy (quad double); for d/dd the TMA-pipelined dataflow kernel
+// (k_mgs_pipe, m a multiple of 256 up to 1024) and otherwise the plain
+// dataflow kernel have the shorter per-sweep latency.
 static int mgs_mode(int nc) {
   const char *v = getenv("PN_MGS_MODE");
   if (v && strcmp(v, "sweeps") == 0) return 2;

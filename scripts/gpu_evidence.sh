@@ -21,10 +21,15 @@ for spec in "mgs:k_mgs_flow" "tree:k_mono_tree" "seg:k_segments" "bsub:k_backsub
   ncu -i /tmp/prof_$name.ncu-rep --page details --csv > $O/${name}_details.csv 2>>$O/$name.err
   ncu -i /tmp/prof_$name.ncu-rep --page raw --csv > $O/${name}_raw.csv 2>>$O/$name.err
 done
+BD="python bench.py --base dd --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $O/launches_cdd.csv $BD > /dev/null 2>$O/launchd.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_mgs_pipe -c 1 -o /tmp/prof_pipe $BD > /dev/null 2>$O/pipe.err
+ncu -i /tmp/prof_pipe.ncu-rep --page details --csv > $O/pipe_details.csv 2>>$O/pipe.err
+ncu -i /tmp/prof_pipe.ncu-rep --page raw --csv > $O/pipe_raw.csv 2>>$O/pipe.err
 C5="python bench.py --batch 296 --dim 256 --terms 256 --base dd --steps 1 --warmup 1 --max-iters 2"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv --log-file $O/launches_c5.csv $C5 > /dev/null 2>$O/launch5.err
 timeout 900 ncu --set full --clock-control none -k regex:k_solve_batch -s 1 -c 1 -o /tmp/prof_solve $C5 > /dev/null 2>$O/solve.err
 ncu -i /tmp/prof_solve.ncu-rep --page details --csv > $O/solve_details.csv 2>>$O/solve.err
 ncu -i /tmp/prof_solve.ncu-rep --page raw --csv > $O/solve_raw.csv 2>>$O/solve.err
-python scripts/ncu_summary.py $O/launches_cqd.csv $O/launches_c5.csv $O/mgs_raw.csv $O/tree_raw.csv $O/seg_raw.csv $O/bsub_raw.csv $O/tail_raw.csv $O/solve_raw.csv > $O/summary.txt 2>&1
+python scripts/ncu_summary.py $O/launches_cqd.csv $O/launches_cdd.csv $O/launches_c5.csv $O/mgs_raw.csv $O/tree_raw.csv $O/seg_raw.csv $O/bsub_raw.csv $O/tail_raw.csv $O/pipe_raw.csv $O/solve_raw.csv > $O/summary.txt 2>&1
 du -sh gpurun_out
