@@ -130,7 +130,7 @@ template <class E, int BASE, int G, class VSink, class DSink>
 __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const int32_t *mv, const int32_t *me,
                                                const E &co, const double *__restrict__ x,
                                                const double *__restrict__ table, const int32_t *__restrict__ toff,
-                                               VSink &&value_sink, DSink &&deriv_sink) {
+                                               VSink &&value_sink, DSink &&deriv_sink, bool unit = false) {
   constexpr int es = Traits<E>::es;
   constexpr int SL = BASE / G;            // slots per lane
   constexpr int NLOC = Log2<SL>::value;   // lane-local levels above the slots
@@ -176,7 +176,9 @@ __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const 
   const E root = X[NX];
 
   // ---- value (evaldiff.py:166-172) ---------------------------------------
-  const E scale = monomial_scale<E>(co, 0, k, mv, me, table, toff);
+  // unit: every exponent is 1 (the bucket was checked on upload), so the
+  // common factor is empty and scale == co
+  const E scale = unit ? co : monomial_scale<E>(co, 0, k, mv, me, table, toff);
   if (active && r == 0) value_sink(emul(scale, root));
 
   // ---- downward sweep of complements (evaldiff.py:89-98) -----------------
@@ -224,13 +226,13 @@ __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const 
       const int t2 = BASE + t;
       const E g1 = emul(cl[u], leaf(t2));
       const E g2 = emul(cl[u], leaf(t));
-      const int d1 = me[t], d2 = me[t2];
+      const int d1 = unit ? 1 : me[t], d2 = unit ? 1 : me[t2];
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
       const E s2 = d2 == 1 ? scale : emul_int(scale, d2);
       deriv_sink(t, emul(s1, g1));
       deriv_sink(t2, emul(s2, g2));
     } else {
-      const int d1 = me[t];
+      const int d1 = unit ? 1 : me[t];
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
       deriv_sink(t, emul(s1, cl[u]));
     }
@@ -459,12 +461,15 @@ __global__ void __launch_bounds__(NT) k_mono_tree_tma(const int32_t *__restrict_
                                                       const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                                                       const double *__restrict__ x, const double *__restrict__ table,
                                                       const int32_t *__restrict__ toff, double *__restrict__ contrib,
-                                                      BView bv) {
+                                                      BView bv, int KS, bool unit) {
   constexpr int es = Traits<E>::es;
   constexpr int CH = NT / G;
   extern __shared__ __align__(16) int tma_smem[];
   __shared__ __align__(8) uint64_t bar[2];
-  const int L = CH * K;                        // ints per array per stage (multiple of 4)
+  // KS: shared-memory row stride of a monomial's support.  KS == K: the chunk
+  // arrives as one contiguous copy per array; otherwise (KS = G mod 32) row by
+  // row, so the 32/G monomials of a warp read distinct banks.
+  const int L = CH * KS;                       // ints per array per stage (multiple of 4)
   int *st_var = tma_smem;                      // [2][L]
   int *st_exp = st_var + 2 * L;                // [2][L]
   int *st_dst = st_exp + 2 * L;                // [2][L]
@@ -483,38 +488,55 @@ __global__ void __launch_bounds__(NT) k_mono_tree_tma(const int32_t *__restrict_
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](long long ch, int s) {  // thread 0: stage chunk ch into buffer s
+  auto issue = [&](long long ch, int s) {  // warp 0: stage chunk ch into buffer s
     const long long m0 = ch * CH;
     const int cnt = (int)min((long long)CH, count - m0);
-    const uint32_t sb = (uint32_t)(((long long)cnt * K * 4 + 15) & ~15LL);
     const uint32_t lb = (uint32_t)((cnt * 4 + 15) & ~15);
     const long long ebeg = e0 + m0 * K;
-    mbar_expect_tx(&bar[s], 3 * sb + lb);
-    bulk_g2s(st_var + s * L, var + ebeg, sb, &bar[s]);
-    bulk_g2s(st_exp + s * L, exps + ebeg, sb, &bar[s]);
-    bulk_g2s(st_dst + s * L, dst + ebeg, sb, &bar[s]);
-    bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
+    if (KS == K) {
+      if (tid == 0) {
+        const uint32_t sb = (uint32_t)(((long long)cnt * K * 4 + 15) & ~15LL);
+        mbar_expect_tx(&bar[s], 3 * sb + lb);
+        bulk_g2s(st_var + s * L, var + ebeg, sb, &bar[s]);
+        bulk_g2s(st_exp + s * L, exps + ebeg, sb, &bar[s]);
+        bulk_g2s(st_dst + s * L, dst + ebeg, sb, &bar[s]);
+        bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
+      }
+      return;
+    }
+    const uint32_t rb = (uint32_t)K * 4;  // K % 4 == 0
+    if (tid == 0) {
+      mbar_expect_tx(&bar[s], 3 * cnt * rb + lb);
+      bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
+    }
+    __syncwarp();
+    for (int i = tid; i < 3 * cnt; i += 32) {
+      const int a = i / cnt, u = i - a * cnt;
+      const int32_t *src = (a == 0 ? var : a == 1 ? exps : dst) + ebeg + (long long)u * K;
+      int *d = (a == 0 ? st_var : a == 1 ? st_exp : st_dst) + s * L + u * KS;
+      bulk_g2s(d, src, rb, &bar[s]);
+    }
   };
   long long ch = blockIdx.x;
-  if (ch < nchunks && tid == 0) issue(ch, 0);
+  if (ch < nchunks && tid < 32) issue(ch, 0);
   uint32_t phase[2] = {0, 0};
   for (int s = 0; ch < nchunks; ch += gridDim.x, s ^= 1) {
     const long long nxt = ch + gridDim.x;
-    if (nxt < nchunks && tid == 0) issue(nxt, s ^ 1);  // buffer s^1 was released by the last barrier
+    if (nxt < nchunks && tid < 32) issue(nxt, s ^ 1);  // buffer s^1 was released by the last barrier
     mbar_wait(&bar[s], phase[s]);
     phase[s] ^= 1;
     const long long m0 = ch * CH;
     const int u = tid / G, r = tid % G;
     const bool active = m0 + u < count;
     const int uu = active ? u : 0;
-    const int *mv = st_var + s * L + uu * K;
-    const int *me = st_exp + s * L + uu * K;
-    const int *md = st_dst + s * L + uu * K;
+    const int *mv = st_var + s * L + uu * KS;
+    const int *me = st_exp + s * L + uu * KS;
+    const int *md = st_dst + s * L + uu * KS;
     const int c = st_lst[s * CH + uu];
     const E co = eload<E>(coeff + (long long)c * es);
     mono_tree_eval<E, BASE, G>(
         r, active, K, mv, me, co, x, table, toff, [&](const E &v) { estore(contrib + (long long)c * es, v); },
-        [&](int t, const E &v) { estore(contrib + (long long)md[t] * es, v); });
+        [&](int t, const E &v) { estore(contrib + (long long)md[t] * es, v); }, unit);
     __syncthreads();  // buffer s is free for the chunk after next
   }
 }
@@ -682,7 +704,16 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
   const bool tma = tv ? strcmp(tv, "0") != 0 : Traits<E>::nc >= 2;
   if (b.dense_k && tma) {
     constexpr int CH = NT / G;
-    const size_t smem = (size_t)(6 * CH * b.dense_k + 2 * CH) * sizeof(int);
+    // PN_TREE_PAD=1: padded row stride KS = G (mod 32), rows copied one by
+    // one (16-byte rows).  Removes the 4-way bank conflicts of the support
+    // reads (ncu: 3.5e8 -> 3.9e6 on C5) but the per-row bulk copies cost more
+    // than the conflicts (C5 4158 -> 3900 start-iter/s, cqd eval 11.8 ->
+    // 12.2 ms), so the contiguous layout is the default.
+    const char *pv = getenv("PN_TREE_PAD");
+    int KS = b.dense_k;
+    if (pv && strcmp(pv, "1") == 0 && G % 4 == 0 && b.dense_k % 4 == 0)
+      while (KS % 32 != G % 32) ++KS;
+    const size_t smem = (size_t)(6 * CH * KS + 2 * CH) * sizeof(int);
     auto kern = k_mono_tree_tma<E, BASE, G, NT>;
     if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -692,7 +723,7 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
     const long long want = std::max(1LL, (long long)std::max(per_sm, 1) * num_sms() / std::max(nb, 1));
     const dim3 grid((unsigned)std::min(nchunks, want), (unsigned)nb);
     kern<<<grid, NT, smem, st>>>(b.d_list, b.count, b.dense_k, b.e0, sys->d_var, sys->d_exp, sys->d_dst, sys->d_coeff,
-                                 x, table, sys->d_toff, contrib, bv);
+                                 x, table, sys->d_toff, contrib, bv, KS, b.unit_exp);
     PN_CHECK_LAUNCH();
     count_launch(1);
     return;

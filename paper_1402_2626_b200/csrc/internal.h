@@ -166,6 +166,7 @@ struct pn_system {
     // (lets k_mono_tree_tma stage whole chunks with bulk copies); 0 if not
     int dense_k = 0;
     long long e0 = 0;
+    bool unit_exp = false;  // dense bucket whose exponents are all 1
   };
   std::vector<Bucket> buckets;
 

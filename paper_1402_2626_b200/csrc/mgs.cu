@@ -402,7 +402,10 @@ struct SmemCol {
   double *base;  // es planes of NT*B doubles
   int plane;
   __device__ __forceinline__ int pos(int r) const {
-    constexpr int W = (32 / B) > 0 ? 32 / B : 1;
+    // a 64-bit warp access is served per half-warp (16 doubles = 32 banks):
+    // XOR the in-block index with the thread's position among the 16/B
+    // threads that share a wavefront's bank row
+    constexpr int W = (16 / B) > 0 ? 16 / B : 1;
     const int t = r / B, i = r % B;
     return t * B + (i ^ ((t / W) % B));
   }

@@ -321,6 +321,9 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
       if (dense) {
         bk.dense_k = K;
         bk.e0 = cptr[L[0]];
+        bool unit = true;
+        for (int64_t t = bk.e0; unit && t < bk.e0 + bk.count * K; ++t) unit = cexp[t] == 1;
+        bk.unit_exp = unit;
       }
     }
     S.buckets.push_back(bk);
