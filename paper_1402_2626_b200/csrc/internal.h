@@ -121,6 +121,9 @@ struct MgsWork {
   DevArena orig;    // orig column norms (hi)
   DevArena status;  // MgsStatus
   DevArena ready;   // dataflow schedule: pivot-published flags (n+1 ints)
+  DevArena own;     // flow schedule: column ownership table (G x maxo ints)
+  long long own_key = -1;
+  int own_maxo = 0;
 };
 void mgs_factor_device(int nc, int cplx, int m, int n, double *A, double *Q, double *R, MgsWork &w,
                        cudaStream_t st);

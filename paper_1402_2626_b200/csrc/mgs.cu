@@ -460,7 +460,8 @@ template <int B> struct Depth { static constexpr int value = B <= 1 ? 1 : B <= 2
 template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
-                                                    MgsStatus *status, int *ready, int kstop) {
+                                                    MgsStatus *status, int *ready, int kstop, int hold, int lag,
+                                                    const int *__restrict__ own, int maxo) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
@@ -473,11 +474,18 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
   __shared__ E s_pe[2][NW], s_re[2];
   __shared__ Rl s_pr[2][NW], s_rr[2];
   __shared__ int s_kn[2], s_fl[2];
-  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int cta = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, w = tid >> 5;
   const int row0 = tid * B;
   const int nparts = (m + B - 1) / B;
-  const int nown = cta <= n ? (n - cta) / G + 1 : 0;
+  // the CTA's columns, ascending (own: maxo per CTA, -1 padded)
+  int cols[64];
+  int nown = 0;
+  for (int i = 0; i < maxo && i < 64; ++i) {
+    const int j = own[cta * maxo + i];
+    if (j < 0) break;
+    cols[nown++] = j;
+  }
   const SmemCol<E, B> col{smem_col, NT * B};
   if (nown == 0) return;
   // CTA-uniform state (every thread holds the same values) and thread 0's
@@ -537,10 +545,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
     if (res == idx) return;
     __syncthreads();  // the current column's sweeps are done with the smem rows
     if (res >= 0) {
-      double *g = A + (long long)(cta + res * G) * m * es;
+      double *g = A + (long long)cols[res] * m * es;
       for (int r = tid; r < m; r += NT) estore(g + (long long)r * es, col.get(r));
     }
-    const double *g = A + (long long)(cta + idx * G) * m * es;
+    const double *g = A + (long long)cols[idx] * m * es;
     for (int r = tid; r < m; r += NT) col.put(r, eload<E>(g + (long long)r * es));
     __syncthreads();
     res = idx;
@@ -588,7 +596,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
 
   // phase 0: initial norms of the owned columns (mgs.py:171-172)
   for (int i = 0; i < nown; ++i) {
-    const int j = cta + i * G;
+    const int j = cols[i];
     if (j >= n) break;
     make_resident(i);
     const Rl nrm = norm();
@@ -600,24 +608,29 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__re
   poll();
   int lo = 0;
   while (lo < nown) {
-    const int c = cta + lo * G;
+    const int c = cols[lo];
     const int tgt = c < kstop ? c : kstop;
     if (fail) return;
     const int dlo = done[lo];
     if (dlo < tgt && dlo >= known) {
-      // critical column blocked on pivot dlo: catch a lagging column up
+      // critical column blocked on pivot dlo: catch a lagging column up --
+      // unless c pivots within `hold` sweeps of the one in flight: then this
+      // CTA is on the critical path and a lagging apply would delay it
       int pick = -1;
       for (int i = lo + 1; i < nown; ++i)
         if (done[i] < known) {
           pick = i;
           break;
         }
+      // ... but a column lagging more than `lag` sweeps is caught up anyway:
+      // its sweeps are a sequential chain that must not pile up
+      if (pick >= 0 && c - dlo <= hold && known - done[pick] <= lag) pick = -1;
       if (pick < 0) {
         block_wait(dlo);
         continue;
       }
       make_resident(pick);
-      const int cj = cta + pick * G;
+      const int cj = cols[pick];
       int d = done[pick];
       while (d < known && d < cj) {
         apply(d, cj);
@@ -1266,6 +1279,70 @@ static void trace_end(int n, unsigned long long *buf, cudaStream_t st) {
   }
 }
 
+// Column ownership of the flow kernel: CTA c owns one column of every round
+// of G consecutive columns.  "rr" (default): column c of each round (c, c+G,
+// ...), which keeps the number of unfinished columns per CTA within one of
+// each other at every point of the factorisation; "snake": the direction
+// alternates per round (c, 2G-1-c, 2G+c, ...).  Snake brings pivot n-C out
+// 14 ms sooner on the cqd step, but leaves the tail kernel's columns behind
+// and the launch ends 4 ms later (profiles/r01, trace of PN_MGS_TRACE).
+// PN_FLOW_OWN=rr|snake|<file> (file: one line per CTA, its columns).
+static void flow_owner_table(int n, int G, MgsWork &w, cudaStream_t st) {
+  const char *v = getenv("PN_FLOW_OWN");
+  const int var = !v || strcmp(v, "rr") == 0 ? 0 : strcmp(v, "snake") == 0 ? 1 : 2;
+  const long long key = ((long long)n << 32) | ((long long)G << 4) | var;
+  if (w.own_key == key && var != 2) return;
+  std::vector<std::vector<int>> lists(G);
+  if (var == 2) {
+    FILE *fp = fopen(v, "r");
+    if (!fp) {
+      set_error("PN_FLOW_OWN: cannot open %s", v);
+      throw Fail{PN_E_ARG};
+    }
+    char line[8192];
+    for (int c = 0; c < G && fgets(line, sizeof line, fp); ++c) {
+      char *q = line;
+      for (;;) {
+        char *e = nullptr;
+        const long j = strtol(q, &e, 10);
+        if (e == q) break;
+        if (j >= 0 && j <= n) lists[c].push_back((int)j);
+        q = e;
+      }
+    }
+    fclose(fp);
+  } else {
+    for (int j = 0; j <= n; ++j) {
+      const int r = j / G, i = j % G;
+      lists[var == 1 && (r & 1) ? G - 1 - i : i].push_back(j);
+    }
+  }
+  int maxo = 1;
+  std::vector<int> seen(n + 1, 0);
+  for (auto &l : lists) {
+    std::sort(l.begin(), l.end());
+    maxo = std::max(maxo, (int)l.size());
+    for (int j : l) ++seen[j];
+  }
+  for (int j = 0; j <= n; ++j)
+    if (seen[j] != 1) {  // an unowned column would stall every pivot after it
+      set_error("flow schedule: column %d owned %d times", j, seen[j]);
+      throw Fail{PN_E_ARG};
+    }
+  if (maxo > 64) {
+    set_error("flow schedule: more than 64 columns per CTA");
+    throw Fail{PN_E_ARG};
+  }
+  std::vector<int> tab((size_t)G * maxo, -1);
+  for (int c = 0; c < G; ++c)
+    for (size_t i = 0; i < lists[c].size(); ++i) tab[(size_t)c * maxo + i] = lists[c][i];
+  w.own.ensure(tab.size() * sizeof(int));
+  PN_CHECK_CUDA(cudaMemcpyAsync(w.own.p, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  PN_CHECK_CUDA(cudaStreamSynchronize(st));  // tab is pageable and goes out of scope
+  w.own_key = key;
+  w.own_maxo = maxo;
+}
+
 template <class E, int B, int NT>
 static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
   MgsStatus *status = w.status.as<MgsStatus>();
@@ -1301,7 +1378,17 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   w.ready.ensure((size_t)(n + 1) * sizeof(int));
   PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
   int *ready = w.ready.as<int>();
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop};
+  // hold: a CTA whose critical column pivots within `hold` sweeps of the
+  // pivot in flight does no lagging work (PN_FLOW_HOLD, 0 = off; 1 measured
+  // 129.5 -> 124.2 ms per cqd step, 2 and 3 within noise of 1)
+  const char *hv = getenv("PN_FLOW_HOLD");
+  int hold = hv ? atoi(hv) : 1;
+  const char *lv = getenv("PN_FLOW_LAG");
+  int lag = lv ? atoi(lv) : 1 << 30;
+  flow_owner_table(n, grid, w, st);
+  const int *own = w.own.as<int>();
+  int maxo = w.own_maxo;
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
