@@ -355,7 +355,7 @@ def run_ours(args):
                 "peak_source": "measured in-run DFMA probe (pn_fp64_peak); MEASURED_PEAKS.json has no FP64 entry",
                 "work_fp64_instr": w_factor, "seconds": t_fac,
                 "arithmetic_ceiling_frac": {4: 0.76, 2: 0.95}.get(nc)}
-    bsub = {"kernel": "k_backsub_lanes" if nc == 4 else "k_backsub_blocked", "seconds": t_solve - t_fac,
+    bsub = {"kernel": "k_backsub_look" if nc == 4 else "k_backsub_blocked_look", "seconds": t_solve - t_fac,
             "work_fp64_instr": w_bsub, "bound": "latency (n dependent divisions)"}
     evalr = {"kernel": "k_mono_tree + k_segments (eval+diff phase)", "seconds": t_eval,
              "achieved_fp64": w_eval / t_eval / 1e12, "frac_fp64": w_eval / t_eval / fp64_peak,

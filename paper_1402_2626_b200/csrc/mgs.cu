@@ -458,7 +458,7 @@ struct Pairwise {
 template <int B> struct Depth { static constexpr int value = B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 3 : B <= 8 ? 4 : 5; };
 
 template <class E, int B, int NT>
-__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
+__global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
                                                     MgsStatus *status, int *ready, int kstop, int hold, int lag,
                                                     const int *__restrict__ own, int maxo) {
@@ -1465,6 +1465,11 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     if constexpr (B == 8) {
       if (m <= 1536 && flow_launch<E, B, 192>(m, n, A, Q, R, w, st)) return;
     }
+    // PN_FLOW_NT=128: 4 warps x 8 rows, three CTAs per SM (m <= 1024)
+    if constexpr (B == 4) {
+      const char *fv = getenv("PN_FLOW_NT");
+      if (fv && atoi(fv) == 128 && flow_launch<E, 8, 128>(m, n, A, Q, R, w, st)) return;
+    }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
   if (mode <= 1 || mode == 4) {
@@ -1522,7 +1527,8 @@ void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStr
 template <class E, int NT>
 __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict__ R, int n, double *__restrict__ x,
                                                         RDiv<Traits<E>::nc> *__restrict__ prep,
-                                                        double *__restrict__ y, int *sing, MgsStatus *status) {
+                                                        double *__restrict__ y, int *sing, MgsStatus *status,
+                                                        int unroll) {
   namespace cg = cooperative_groups;
   using RD = RDiv<Traits<E>::nc>;
   constexpr int es = Traits<E>::es;
@@ -1589,12 +1595,28 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict
       for (int jj = 0; jj < hi - lo; ++jj) sU[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + r) * es);
       yr = eload<E>(y + (long long)r * es);
       __syncwarp();
-      for (int j = hi - 1; j >= lo; --j) yr = esub(yr, emul(sU[(j - lo) * 32 + lane], sX[j - lo]));
+      if (unroll) {
+        const int nbk = hi - lo;
+#pragma unroll 8
+        for (int jj = 31; jj >= 0; --jj)
+          if (jj < nbk) yr = esub(yr, emul(sU[jj * 32 + lane], sX[jj]));
+      } else {
+        for (int j = hi - 1; j >= lo; --j) yr = esub(yr, emul(sU[(j - lo) * 32 + lane], sX[j - lo]));
+      }
     } else {
       const int worker = blockIdx.x == 0 ? threadIdx.x - 32 : gtid - 32;
       const int workers = gsize - 32;
       for (int r = worker; r < lo - 32; r += workers) {
         E v = eload<E>(y + (long long)r * es);
+        if (unroll) {
+          const int nbk = hi - lo;
+#pragma unroll 4
+          for (int jj = 31; jj >= 0; --jj)
+            if (jj < nbk)
+              v = esub(v, emul(eload<E>(R + ((long long)(lo + jj) * ld + r) * es), eload<E>(x + (long long)(lo + jj) * es)));
+          estore(y + (long long)r * es, v);
+          continue;
+        }
         E rn = eload<E>(R + ((long long)(hi - 1) * ld + r) * es);
         for (int j = hi - 1; j >= lo; --j) {
           const E rc = rn;
@@ -1665,7 +1687,7 @@ __device__ __forceinline__ C<NC> lp_div(const C<NC> &yv, const C<NC> &r, const R
 template <int NC, int NT>
 __global__ void __launch_bounds__(NT) k_backsub_lanes(const double *__restrict__ R, int n, double *__restrict__ x,
                                                       RDiv<NC> *__restrict__ prep, double *__restrict__ y,
-                                                      int *sing, MgsStatus *status) {
+                                                      int *sing, MgsStatus *status, int unroll) {
   namespace cg = cooperative_groups;
   using E = C<NC>;
   constexpr int es = 2 * NC;
@@ -1736,18 +1758,276 @@ __global__ void __launch_bounds__(NT) k_backsub_lanes(const double *__restrict__
       }
       __syncthreads();
       E v = eload<E>(y + (long long)r * es);
-      for (int j = hi - 1; j >= lo; --j) v = lp_csub(v, lp_cmul(sU[(j - lo) * 32 + rl], sX[j - lo], p, g4), p, g4);
+      // unrolled: the products are independent of v, only the subtractions
+      // chain (PN_BACKSUB_UNROLL=0: the plain loop, for comparison)
+      if (unroll) {
+#pragma unroll 8
+        for (int jj = 31; jj >= 0; --jj)
+          if (jj < nbk) v = lp_csub(v, lp_cmul(sU[jj * 32 + rl], sX[jj], p, g4), p, g4);
+      } else {
+        for (int j = hi - 1; j >= lo; --j) v = lp_csub(v, lp_cmul(sU[(j - lo) * 32 + rl], sX[j - lo], p, g4), p, g4);
+      }
       if (p == 0) estore(y + (long long)r * es, v);
       __syncthreads();
     } else {
       // all rows above the next block take this block's x
       for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {
         E v = eload<E>(y + (long long)r * es);
-        for (int j = hi - 1; j >= lo; --j)
-          v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+        if (unroll) {
+#pragma unroll 4
+          for (int jj = 31; jj >= 0; --jj)
+            if (jj < nbk)
+              v = esub(v, emul(eload<E>(R + ((long long)(lo + jj) * ld + r) * es), eload<E>(x + (long long)(lo + jj) * es)));
+        } else {
+          for (int j = hi - 1; j >= lo; --j)
+            v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
+        }
         estore(y + (long long)r * es, v);
       }
     }
+  }
+}
+
+// k_backsub_look: k_backsub_lanes with the next block's rows updated inside
+// the solve.  CTA 0 has two 128-thread groups: the solver (rows of block b,
+// four lanes per row) and a lookahead group holding the 32 rows of block b-1,
+// which subtracts R[i, j] x_j for each x_j of block b as soon as the solver
+// has it (two updates per solver step), after first catching up on block
+// b+1's x.  The other CTAs apply block b+1's x to every row below block b-1
+// meanwhile.  Every row still takes its updates in descending j (blocks b+2..
+// from the other CTAs in earlier rounds, then b+1 and b from the lookahead
+// group), so x is bit-identical to k_backsub_lanes; the solver no longer
+// waits for a separate next-block pass (mgs.py:229-247).
+template <int NC>
+__global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__ R, int n, double *__restrict__ x,
+                                                      RDiv<NC> *__restrict__ prep, double *__restrict__ y,
+                                                      int *sing, MgsStatus *status) {
+  namespace cg = cooperative_groups;
+  using E = C<NC>;
+  constexpr int es = 2 * NC;
+  constexpr int NT = 256;
+  extern __shared__ __align__(16) double lk_smem[];
+  E *sD = reinterpret_cast<E *>(lk_smem);  // R[lo+ii, lo+jj] at jj*32+ii (diagonal block b)
+  E *sU = sD + 32 * 32;                     // R[lo-32+ii, lo+jj]    (block b-1 rows, block b columns)
+  E *sV = sU + 32 * 32;                     // R[lo-32+ii, lo+32+jj] (block b-1 rows, block b+1 columns)
+  E *sX = sV + 32 * 32;                     // [2][32]: x of block b at parity b & 1
+  E *sY = sX + 64;                          // block b-1 rows after the lookahead
+  RDiv<NC> *sP = reinterpret_cast<RDiv<NC> *>(sY + 32);
+  __shared__ int s_step[1];  // solver steps whose x_j is in sX
+  cg::grid_group grid = cg::this_grid();
+  if (status->code) return;
+  if (threadIdx.x == 0) s_step[0] = 0;
+  const long long ld = n + 1;
+  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
+  for (int j = gtid; j < n; j += gsize) {
+    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
+    const double *dg = R + ((long long)j * ld + j) * es;
+    bool nz = false;
+#pragma unroll
+    for (int q = 0; q < es; ++q) nz |= dg[q] != 0.0;
+    if (!nz) atomicMax(sing, j);
+    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
+  }
+  grid.sync();
+  if (*(volatile int *)sing >= 0) {
+    if (gtid == 0) {
+      status->k = *sing;
+      status->code = PN_E_SINGULAR;
+    }
+    return;
+  }
+  const int t = threadIdx.x, tt = t & 127, lane = t & 31, p = lane & 3, g4 = lane & ~3;
+  const bool solver = t < 128;
+  const int rl = tt >> 2;
+  const int nb = (n + 31) / 32;
+  for (int b = nb - 1; b >= 0; --b) {
+    const int lo = b * 32, hi = min(n, lo + 32), nbk = hi - lo;
+    const int par = b & 1;
+    if (blockIdx.x == 0) {
+      // catch-up columns (block b+1) and lookahead rows exist only for b > 0
+      const int ncu = (b > 0 && b + 1 < nb) ? min(n, lo + 64) - (lo + 32) : 0;
+      if (solver) {
+        for (int e = tt; e < 32 * 32; e += 128) {
+          const int jj = e >> 5, ii = e & 31;
+          if (jj < nbk && ii <= jj) sD[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo + ii) * es);
+        }
+        if (tt < nbk) sP[tt] = prep[lo + tt];
+      } else if (b > 0) {
+        for (int e = tt; e < 32 * 32; e += 128) {
+          const int jj = e >> 5, ii = e & 31;
+          if (jj < nbk) sU[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + ii) * es);
+          if (jj < ncu) sV[e] = eload<E>(R + ((long long)(lo + 32 + jj) * ld + lo - 32 + ii) * es);
+        }
+      }
+      __syncthreads();
+      E yr = ezero<E>(), v = ezero<E>();
+      if (solver) {
+        if (rl < nbk) yr = b == nb - 1 ? eload<E>(y + (long long)(lo + rl) * es) : sY[rl];
+      } else if (b > 0) {
+        v = eload<E>(y + (long long)(lo - 32 + rl) * es);
+      }
+      int q = 0;  // lookahead group's next update
+      auto look = [&]() {
+        if (q < ncu) {
+          const int jj = ncu - 1 - q;
+          v = lp_csub(v, lp_cmul(sV[jj * 32 + rl], sX[(par ^ 1) * 32 + jj], p, g4), p, g4);
+        } else {
+          const int jj = nbk - 1 - (q - ncu);
+          v = lp_csub(v, lp_cmul(sU[jj * 32 + rl], sX[par * 32 + jj], p, g4), p, g4);
+        }
+        ++q;
+      };
+      __syncthreads();  // sY was read before the lookahead group rewrites it
+      if (solver) {
+        // the solver's steps sync on a named barrier of its 128 threads; the
+        // lookahead group follows the published-step counter instead
+        for (int s = 0; s < nbk; ++s) {
+          const int jl = nbk - 1 - s;
+          if ((jl >> 3) == (tt >> 5)) {
+            const E xj = lp_div(yr, sD[jl * 32 + jl], sP[jl], p, g4);
+            if (rl == jl && p == 0) {
+              sX[par * 32 + jl] = xj;
+              __threadfence_block();
+              *(volatile int *)s_step = s + 1;
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if ((tt >> 5) * 8 < jl) {
+            const E u = lp_csub(yr, lp_cmul(sD[jl * 32 + rl], sX[par * 32 + jl], p, g4), p, g4);
+            if (rl < jl) yr = u;
+          }
+        }
+      } else if (b > 0) {
+        // block b+1's x first, then block b's as the solver publishes them
+        while (q < ncu) look();
+        for (int s = 0; s < nbk; ++s) {
+          while (*(volatile int *)s_step <= s) __nanosleep(20);
+          __threadfence_block();
+          look();
+        }
+        if (p == 0) sY[rl] = v;
+      }
+      __syncthreads();
+      if (t == 0) *(volatile int *)s_step = 0;
+      if (solver && tt < nbk) estore(x + (long long)(lo + tt) * es, sX[par * 32 + tt]);
+    } else if (b + 1 < nb) {
+      // rows below block b-1 take block b+1's x (descending columns)
+      const int c0 = lo + 32, nc1 = min(n, lo + 64) - c0;
+      for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {
+        E v = eload<E>(y + (long long)r * es);
+#pragma unroll 4
+        for (int jj = 31; jj >= 0; --jj)
+          if (jj < nc1)
+            v = esub(v, emul(eload<E>(R + ((long long)(c0 + jj) * ld + r) * es), eload<E>(x + (long long)(c0 + jj) * es)));
+        estore(y + (long long)r * es, v);
+      }
+    }
+    grid.sync();
+  }
+}
+
+// k_backsub_blocked_look: k_backsub_blocked (one lane per row) with the
+// lookahead of k_backsub_look: warp 0 of CTA 0 solves block b, warp 1 holds
+// block b-1's rows, applies block b+1's x and then block b's x_j as warp 0
+// publishes them; the rest of the grid applies block b+1's x to the rows
+// below block b-1.  Same per-row subtraction order as k_backsub_blocked.
+template <class E, int NT>
+__global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__restrict__ R, int n,
+                                                             double *__restrict__ x,
+                                                             RDiv<Traits<E>::nc> *__restrict__ prep,
+                                                             double *__restrict__ y, int *sing, MgsStatus *status) {
+  namespace cg = cooperative_groups;
+  using RD = RDiv<Traits<E>::nc>;
+  constexpr int es = Traits<E>::es;
+  extern __shared__ __align__(16) double bk_smem[];
+  E *sD = reinterpret_cast<E *>(bk_smem);  // R[lo+ii, lo+jj] at jj*32+ii
+  E *sU = sD + 32 * 32;                     // R[lo-32+ii, lo+jj]
+  E *sV = sU + 32 * 32;                     // R[lo-32+ii, lo+32+jj]
+  E *sX = sV + 32 * 32;                     // [2][32]
+  E *sY = sX + 64;                          // block b-1 rows after the lookahead
+  RD *sP = reinterpret_cast<RD *>(sY + 32);
+  __shared__ int s_step[1];
+  cg::grid_group grid = cg::this_grid();
+  if (status->code) return;
+  if (threadIdx.x == 0) s_step[0] = 0;
+  const long long ld = n + 1;
+  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
+  for (int j = gtid; j < n; j += gsize) {
+    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
+    const double *dg = R + ((long long)j * ld + j) * es;
+    bool nz = false;
+#pragma unroll
+    for (int p = 0; p < es; ++p) nz |= dg[p] != 0.0;
+    if (!nz) atomicMax(sing, j);
+    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
+  }
+  grid.sync();
+  if (*(volatile int *)sing >= 0) {
+    if (gtid == 0) {
+      status->k = *sing;
+      status->code = PN_E_SINGULAR;
+    }
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = (n + 31) / 32;
+  for (int b = nb - 1; b >= 0; --b) {
+    const int lo = b * 32, hi = min(n, lo + 32), nbk = hi - lo;
+    const int par = b & 1;
+    if (blockIdx.x == 0) {
+      const int ncu = (b > 0 && b + 1 < nb) ? min(n, lo + 64) - (lo + 32) : 0;
+      if (warp == 0) {
+        for (int jj = 0; jj < nbk; ++jj)
+          if (lane <= jj) sD[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo + lane) * es);
+        if (lane < nbk) sP[lane] = prep[lo + lane];
+      } else if (warp == 1 && b > 0) {
+        for (int jj = 0; jj < nbk; ++jj) sU[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + lane) * es);
+        for (int jj = 0; jj < ncu; ++jj)
+          sV[jj * 32 + lane] = eload<E>(R + ((long long)(lo + 32 + jj) * ld + lo - 32 + lane) * es);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        E yr = ezero<E>();
+        if (lane < nbk) yr = b == nb - 1 ? eload<E>(y + (long long)(lo + lane) * es) : sY[lane];
+        __syncwarp();
+        E xl = ezero<E>();
+        for (int s = 0; s < nbk; ++s) {
+          const int jl = nbk - 1 - s;
+          if (lane == jl) {
+            xl = ediv_with(yr, sD[jl * 32 + jl], sP[jl]);
+            sX[par * 32 + jl] = xl;
+            __threadfence_block();
+            *(volatile int *)s_step = s + 1;
+          }
+          const E xj = eshfl_idx(xl, jl);
+          if (lane < jl) yr = esub(yr, emul(sD[jl * 32 + lane], xj));
+        }
+        if (lane < nbk) estore(x + (long long)(lo + lane) * es, xl);
+      } else if (warp == 1 && b > 0) {
+        E v = eload<E>(y + (long long)(lo - 32 + lane) * es);
+        for (int jj = ncu - 1; jj >= 0; --jj) v = esub(v, emul(sV[jj * 32 + lane], sX[(par ^ 1) * 32 + jj]));
+        for (int s = 0; s < nbk; ++s) {
+          const int jl = nbk - 1 - s;
+          while (*(volatile int *)s_step <= s) __nanosleep(20);
+          __threadfence_block();
+          v = esub(v, emul(sU[jl * 32 + lane], sX[par * 32 + jl]));
+        }
+        sY[lane] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) *(volatile int *)s_step = 0;
+    } else if (b + 1 < nb) {
+      const int c0 = lo + 32, nc1 = min(n, lo + 64) - c0;
+      for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {
+        E v = eload<E>(y + (long long)r * es);
+#pragma unroll 4
+        for (int jj = 31; jj >= 0; --jj)
+          if (jj < nc1)
+            v = esub(v, emul(eload<E>(R + ((long long)(c0 + jj) * ld + r) * es), eload<E>(x + (long long)(c0 + jj) * es)));
+        estore(y + (long long)r * es, v);
+      }
+    }
+    grid.sync();
   }
 }
 
@@ -1760,8 +2040,9 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
   // with lanes (1.18 vs 1.0 ms at n = 1024): its chain is short already.
   if constexpr (Traits<E>::cplx && Traits<E>::nc == 4) {
     constexpr int NC = Traits<E>::nc;
-    if (!(mode && (strcmp(mode, "single") == 0 || strcmp(mode, "blocked") == 0))) {
-      constexpr int NT = 128;
+    // default: the lookahead kernel (3.7 vs 5.2 ms for lanes at n = 1024)
+    if (!mode || strcmp(mode, "look") == 0) {
+      constexpr int NT = 256;
       DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
       DevBuf sbuf(16, st);
       int *sing = sbuf.as<int>();
@@ -1771,6 +2052,25 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
       double *yp = yw.d();
       MgsStatus *status = w.status.as<MgsStatus>();
       void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
+      const size_t smem = (size_t)(3 * 32 * 32 + 96) * es * sizeof(double) + 32 * sizeof(RDiv<NC>);
+      PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_look<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_look<NC>, grid, NT, args, smem, st));
+      count_launch(1);
+      return;
+    }
+    if (strcmp(mode, "lanes") == 0) {
+      constexpr int NT = 128;
+      DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
+      DevBuf sbuf(16, st);
+      int *sing = sbuf.as<int>();
+      PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
+      const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
+      RDiv<NC> *pp = prep.as<RDiv<NC>>();
+      double *yp = yw.d();
+      MgsStatus *status = w.status.as<MgsStatus>();
+      const char *uv = getenv("PN_BACKSUB_UNROLL");
+      int unroll = uv ? atoi(uv) : 1;
+      void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status, &unroll};
       const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<NC>);
       PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_lanes<NC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
@@ -1778,6 +2078,24 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
       count_launch(1);
       return;
     }
+  }
+  if (!mode || strcmp(mode, "look") == 0) {
+    constexpr int NT = 128;
+    DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
+    DevBuf sbuf(16, st);
+    int *sing = sbuf.as<int>();
+    PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
+    const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
+    RDiv<Traits<E>::nc> *pp = prep.as<RDiv<Traits<E>::nc>>();
+    double *yp = yw.d();
+    MgsStatus *status = w.status.as<MgsStatus>();
+    void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
+    const size_t smem = (size_t)(3 * 32 * 32 + 96) * es * sizeof(double) + 32 * sizeof(RDiv<Traits<E>::nc>);
+    auto kern = k_backsub_blocked_look<E, NT>;
+    PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
+    count_launch(1);
+    return;
   }
   if (!(mode && strcmp(mode, "single") == 0)) {
     constexpr int NT = 128;
@@ -1789,7 +2107,9 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
     RDiv<Traits<E>::nc> *pp = prep.as<RDiv<Traits<E>::nc>>();
     double *yp = yw.d();
     MgsStatus *status = w.status.as<MgsStatus>();
-    void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status};
+    const char *uv = getenv("PN_BACKSUB_UNROLL");
+    int unroll = uv ? atoi(uv) : 1;
+    void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status, &unroll};
     const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<Traits<E>::nc>);
     PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_blocked<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
