@@ -56,10 +56,11 @@ def _check(res, ref):
     assert res.z == z
 
 
-@pytest.mark.parametrize("own,hold", [("rr", "0"), ("rr", "3"), ("snake", "1"), ("snake", "0")])
-def test_flow_schedules_bit_identical(gpu, case, own, hold):
+@pytest.mark.parametrize("own,hold,pick", [("rr", "0", "0"), ("rr", "3", "1"), ("snake", "1", "0"),
+                                           ("snake", "0", "1"), ("rr", "1", "0")])
+def test_flow_schedules_bit_identical(gpu, case, own, hold, pick):
     aug, ref = case
-    with env(PN_MGS_MODE="flow", PN_FLOW_OWN=own, PN_FLOW_HOLD=hold):
+    with env(PN_MGS_MODE="flow", PN_FLOW_OWN=own, PN_FLOW_HOLD=hold, PN_FLOW_PICK=pick):
         _check(_solve(aug), ref)
 
 
