@@ -10,7 +10,8 @@ C ABI in ``include/polynewt_b200.h``.  There is no CPU fallback.
 
 from .xprec import (Complex, DomainError, DoubleDouble, PrecisionLevel, QuadDouble,
                     precision_level)
-from .polyrep import Monomial, PackedSystem, PolySystem, decompose
+from .polyrep import (Monomial, PackedSystem, PolySystem, SystemParseError, decompose, parse_system,
+                      serialize_system)
 from .evaldiff import OpCounter, PreparedSystem, SystemEvaluation, evaluate_system
 from .mgs import (AugmentedMatrix, LeastSquaresResult, MgsBreakdownError, QRFactors,
                   SingularMatrixError, TilingConfig, back_substitute, back_substitute_staged,
@@ -26,8 +27,8 @@ __all__ = [
     "QuadDouble", "SingularMatrixError", "SystemEvaluation", "TilingConfig", "TraceEntry",
     "VecContext", "back_substitute", "back_substitute_staged", "convergence_ratio",
     "decompose", "evaluate_system", "homotopy_start_system", "inf_norm",
-    "least_squares_solve", "mgs_qr", "mgs_qr_delayed", "newton_step", "precision_level",
-    "promote", "run_newton",
+    "least_squares_solve", "mgs_qr", "mgs_qr_delayed", "newton_step", "parse_system", "precision_level",
+    "promote", "run_newton", "serialize_system", "SystemParseError",
 ]
 
 __version__ = "0.1.0"

@@ -10,6 +10,7 @@ no per-monomial Python objects are needed at benchmark scale.
 
 from __future__ import annotations
 
+import re
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -182,3 +183,167 @@ class PowerTable:
 
     def get(self, var: int, d: int):
         return self.powers[var][d]
+
+
+# ---------------------------------------------------------------------------
+# System text format (polyrep.py:140-304).  Line 1 is "m n"; then m
+# polynomials, each a '+'/'-'-separated list of terms closed by ';'.  A term
+# is a '*'-product of at most one coefficient ("2.5", ".5", "(re,im)") and
+# variable factors "x<i>" / "x<i>^<d>" (repeated variables add exponents;
+# the coefficient defaults to one).  Errors carry the 1-based line and column
+# of the offending character, exactly as the reference reports them.
+
+class SystemParseError(ValueError):
+    """Malformed system text (polyrep.py:16-20)."""
+
+    def __init__(self, line: int, col: int, message: str):
+        super().__init__(f"line {line}, column {col}: {message}")
+        self.line = line
+        self.col = col
+
+
+# factor grammar: a variable, a parenthesised complex literal, or a number
+# (digits, '.', '_', exponent letters and signs run greedily, so "3-x0" is
+# one malformed number -- the reference's tokenizer behaves the same way)
+_VAR_RE = re.compile(r"x(\d+)(?:\^(\d+))?")
+_CPLX_RE = re.compile(r"\([^()]*\)")
+_NUM_RE = re.compile(r"\.?[0-9][0-9_.eE+-]*")
+_SIGNS = "+-−"
+
+
+def _render_term(level: PrecisionLevel, coeff, exponents) -> str:
+    return level.render(coeff) + "".join(f"*x{v}" + (f"^{d}" if d > 1 else "") for v, d in exponents)
+
+
+def serialize_system(system: PolySystem, level: PrecisionLevel) -> str:
+    """Text of the canonicalised system (polyrep.py:150-166).  Real levels
+    write negative non-leading coefficients as " - |c|"."""
+    out = [f"{system.n_eqs} {system.n_vars}"]
+    for poly in system.canonicalized().polys:
+        text = ""
+        for i, mon in enumerate(poly):
+            coeff = mon.coeff
+            if i == 0:
+                sep = ""
+            elif not level.cplx and level.to_components(coeff)[0] < 0.0:
+                sep, coeff = " - ", -coeff  # the sign of a normalised value is its leading component's
+            else:
+                sep = " + "
+            text += sep + _render_term(level, coeff, mon.exponents)
+        out.append(text + ";")
+    return "\n".join(out) + "\n"
+
+
+class _Text:
+    """Cursor over the system text with reference-compatible error positions."""
+
+    def __init__(self, text: str):
+        self.s = text
+        self.i = 0
+
+    def fail(self, message: str, at: int | None = None):
+        p = self.i if at is None else at
+        line = self.s.count("\n", 0, p) + 1
+        col = p - self.s.rfind("\n", 0, p)
+        raise SystemParseError(line, col, message)
+
+    def next_char(self) -> str:
+        """First non-blank character from the cursor ('' at the end); the
+        cursor moves past the blanks."""
+        s, i = self.s, self.i
+        while i < len(s) and s[i].isspace():
+            i += 1
+        self.i = i
+        return s[i] if i < len(s) else ""
+
+
+def parse_system(text: str, level: PrecisionLevel) -> PolySystem:
+    """Inverse of serialize_system for any spacing (polyrep.py:190-207)."""
+    cur = _Text(text)
+    head = text.split("\n", 1)[0].split()
+    if len(head) != 2:
+        cur.fail("expected header line 'm n'")
+    try:
+        m, n_vars = int(head[0]), int(head[1])
+    except ValueError:
+        cur.fail("expected integer equation and variable counts")
+    nl = text.find("\n")
+    cur.i = len(text) if nl < 0 else nl + 1
+    polys = [_read_poly(cur, level, n_vars) for _ in range(m)]
+    if cur.next_char():
+        cur.fail("trailing input after the last polynomial")
+    return PolySystem(n_vars, polys)
+
+
+def _read_poly(cur: _Text, level: PrecisionLevel, n_vars: int) -> list:
+    """Terms up to ';' (polyrep.py:210-238)."""
+    terms = []
+    sign = None      # pending sign character, not yet followed by a term
+    started = False  # any sign or term seen
+    while True:
+        ch = cur.next_char()
+        if not ch:
+            cur.fail("unexpected end of input, expected ';'")
+        if ch == ";":
+            if sign is not None:
+                cur.fail("expected a term after the sign")
+            cur.i += 1
+            if not started:
+                cur.fail("empty polynomial")
+            return terms
+        if ch in _SIGNS:
+            if sign is not None:
+                cur.fail("expected a term after the sign")
+            cur.i += 1
+            sign, started = ch, True
+            continue
+        if terms and sign is None:
+            cur.fail("expected '+', '-' or ';' between terms")
+        terms.append(_read_term(cur, level, n_vars, negate=sign is not None and sign != "+"))
+        sign, started = None, True
+
+
+def _read_term(cur: _Text, level: PrecisionLevel, n_vars: int, negate: bool):
+    """One '*'-product of factors (polyrep.py:241-294)."""
+    coeff = None
+    powers: dict = {}
+    while True:
+        cur.next_char()
+        at, s = cur.i, cur.s
+        mv = _VAR_RE.match(s, at)
+        if mv:
+            idx = int(mv.group(1))
+            if not 0 <= idx < n_vars:
+                cur.fail(f"variable index {idx} out of range (n={n_vars})", at)
+            d = int(mv.group(2)) if mv.group(2) else 1
+            if d < 1:
+                cur.fail("exponents must be >= 1", at)
+            powers[idx] = powers.get(idx, 0) + d
+            end = mv.end()
+        else:
+            mc = _CPLX_RE.match(s, at)
+            mn = None if mc else _NUM_RE.match(s, at)
+            tok = mc or mn
+            if tok is None:
+                cur.fail("expected a coefficient or variable factor")
+            if coeff is not None:
+                cur.fail("duplicate coefficient", at)
+            try:
+                coeff = level.parse(tok.group(0))
+            except Exception:
+                cur.fail("malformed complex coefficient" if mc else "malformed numeric coefficient", at)
+            end = tok.end()
+        cur.i = end
+        if cur.next_char() != "*":
+            break
+        cur.i += 1
+    if cur.next_char() == "^":  # "x0^": the exponent digits are missing
+        cur.fail("malformed exponent")
+    if coeff is None:
+        coeff = level.one()
+    if negate:
+        coeff = -coeff
+    try:
+        return Monomial(coeff, tuple(sorted(powers.items())))
+    except ValueError as exc:
+        cur.fail(str(exc))
