@@ -31,6 +31,16 @@ def raw(path):
     st = [(k, d[k]) for k in h if k.startswith('smsp__average_warps_issue_stalled_') and k.endswith('_per_issue_active.ratio')]
     st.sort(key=lambda kv: -float(kv[1].replace(',', '') or 0))
     print("stalls/issue:", ", ".join(f"{k[34:-23]}={float(x):.2f}" for k, x in st[:8]))
+    # executed FP64 thread instructions (predicated-on lanes only), to set
+    # against the algorithmic work model of bench.work_counts
+    try:
+        cyc = float(d['smsp__cycles_elapsed.avg'].replace(',', ''))
+        fp = {op: float(d[f'smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed'].replace(',', '')) * cyc
+              for op in ('dadd', 'dmul', 'dfma')}
+        print("  fp64 thread instr: " + ", ".join(f"{k}={v:.4g}" for k, v in fp.items())
+              + f", total={sum(fp.values()):.4g}")
+    except (KeyError, ValueError):
+        pass
     for key in ['gpu__time_duration.sum', 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
                 'sm__warps_active.avg.per_cycle_active', 'launch__registers_per_thread', 'launch__grid_size',
                 'launch__block_size', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
