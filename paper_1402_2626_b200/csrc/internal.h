@@ -194,6 +194,16 @@ struct pn_system {
   pn::MgsWork mgs;
   cudaEvent_t ev = nullptr;
 
+  // CUDA graph of the device part of pn_newton_step (evaluation,
+  // factorisation, back substitution, update) for small systems, where the
+  // step is launch-bound: captured after the first direct step, replayed
+  // afterwards.  graph_state: 0 not tried, 1 captured, -1 capture refused
+  cudaGraphExec_t step_graph = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t gev[5] = {};
+  long long graph_launches = 0;  // kernels inside the graph (launch counter)
+  int graph_state = 0;
+
   ~pn_system();
 };
 

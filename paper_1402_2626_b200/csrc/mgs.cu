@@ -1243,6 +1243,7 @@ static int mgs_mode(int nc) {
   if (v && strcmp(v, "flow") == 0) return 0;
   if (v && strcmp(v, "warp") == 0) return 3;
   if (v && strcmp(v, "pipe") == 0) return 4;
+  if (v && strcmp(v, "small") == 0) return 5;
   return nc == 4 ? 0 : 4;
 }
 
@@ -1447,13 +1448,116 @@ static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   return true;
 }
 
+// k_mgs_small: the whole factorisation in one CTA for m <= 32 (config C1
+// and the small systems of the tests).  [A b] sits in shared memory as
+// component planes (row = lane, conflict-free); warp w owns columns w,
+// w + NW, ...; per pivot the owner computes r_kk and q_k, one barrier, every
+// warp sweeps its later columns, one barrier.  Sums over rows are the warp
+// shuffle tree with right pruning = tree_sum's order (mgs.py:145-221); no
+// inter-CTA flags, so a pivot costs its arithmetic chain plus two barriers.
+template <class E>
+__global__ void __launch_bounds__(512) k_mgs_small(const double *__restrict__ A, int m, int n, double eps,
+                                                   double *__restrict__ Q, double *__restrict__ R,
+                                                   MgsStatus *status) {
+  using Rl = typename Traits<E>::R;
+  constexpr int es = Traits<E>::es;
+  extern __shared__ __align__(16) double ms_smem[];
+  __shared__ double s_orig[64];
+  __shared__ int s_fail;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const int ncol = n + 1, P = ncol * 32;
+  auto get = [&](int j) {
+    E v;
+    double *d = reinterpret_cast<double *>(&v);
+#pragma unroll
+    for (int c = 0; c < es; ++c) d[c] = ms_smem[c * P + j * 32 + lane];
+    return v;
+  };
+  auto put = [&](int j, const E &v) {
+    const double *d = reinterpret_cast<const double *>(&v);
+#pragma unroll
+    for (int c = 0; c < es; ++c) ms_smem[c * P + j * 32 + lane] = d[c];
+  };
+  // tree_sum over rows 0..m-1 of one value per lane, result on every lane
+  auto wsum = [&](auto v) {
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const auto o = eshfl_down(v, s);
+      if ((lane & (2 * s - 1)) == 0 && lane + s < m) v = eadd(v, o);
+    }
+    return eshfl_idx(v, 0);
+  };
+  auto norm = [&](int j) -> Rl { return fsqrt(wsum(lane < m ? eabs2(get(j)) : ezero<Rl>())); };
+  if (threadIdx.x == 0) s_fail = 0;
+  for (int j = w; j < ncol; j += NW) put(j, lane < m ? eload<E>(A + ((long long)j * m + lane) * es) : ezero<E>());
+  __syncthreads();
+  for (int j = w; j < n; j += NW) {  // initial column norms (mgs.py:171-172)
+    const Rl nrm = norm(j);
+    if (lane == 0) s_orig[j] = nrm.c[0];
+  }
+  __syncthreads();
+  for (int k = 0; k <= n; ++k) {
+    if (w == k % NW) {  // pivot k (mgs.py:176-193); k == n is the residual norm z
+      const Rl rkk = norm(k);
+      bool ok = true;
+      if (k < n) {
+        const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), s_orig[k]);
+        if (rkk.c[0] <= thr) {
+          ok = false;
+          if (lane == 0) {
+            status->k = k;
+            status->rkk = rkk.c[0];
+            status->thr = thr;
+            status->code = PN_E_BREAKDOWN;
+            s_fail = 1;
+          }
+        }
+      }
+      if (ok) {
+        if (lane == 0) estore(R + ((long long)k * ncol + k) * es, eembed(rkk, (E *)nullptr));
+        if (k < n) {
+          const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+          const E q = ediv_prepared(get(k), p);
+          put(k, q);
+          if (lane < m) estore(Q + ((long long)k * m + lane) * es, q);
+        }
+      }
+    }
+    __syncthreads();
+    if (s_fail || k == n) break;
+    for (int j = w; j < ncol; j += NW) {  // sweep k over the later columns (mgs.py:201-215)
+      if (j <= k) continue;
+      const E q = get(k), a = get(j);
+      const E r = wsum(lane < m ? emul(econj(q), a) : ezero<E>());
+      if (lane < m) put(j, esub(a, emul(q, r)));
+      if (lane == 0) estore(R + ((long long)j * ncol + k) * es, r);
+    }
+    __syncthreads();
+  }
+}
+
 template <class E, int B>
 static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
   MgsStatus *status = w.status.as<MgsStatus>();
   double *orig = w.orig.d();
   const double eps = level_eps(Traits<E>::nc);
   const int sms = num_sms();
-  const int mode = mgs_mode(Traits<E>::nc);
+  int mode = mgs_mode(Traits<E>::nc);
+  // one CTA for m <= 32 (default for d/dd: C1 cd step 0.231 -> 0.176 ms;
+  // qd keeps the dataflow kernel, whose 33 CTAs sweep the columns in
+  // parallel: 1.07 vs 1.14 ms; PN_MGS_MODE=small forces it, larger m take
+  // the default schedule)
+  if (m <= 32 && (mode == 5 || (!getenv("PN_MGS_MODE") && Traits<E>::nc <= 2))) {
+    const size_t smem = (size_t)Traits<E>::es * (n + 1) * 32 * sizeof(double);
+    auto kern = k_mgs_small<E>;
+    if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nt = std::min(512, 32 * (n + 1));
+    kern<<<1, nt, smem, st>>>(A, m, n, eps, Q, R, status);
+    PN_CHECK_LAUNCH();
+    count_launch(1);
+    return;
+  }
+  if (mode == 5) mode = Traits<E>::nc == 4 ? 0 : 4;
   if (mode == 3 && Traits<E>::nc <= 2 && m <= 1024) {
     bool done = false;
     if (m <= 128) done = try_mgs_warp<E, 4>(m, n, A, Q, R, w, st);

@@ -13,6 +13,53 @@
 
 using namespace pn;
 
+// Graph replay of the device step for small systems (PN_GRAPH=1 always, 0
+// never; default m*(n+1) <= 128*129, where the step is a few dozen short,
+// launch-bound kernels).  The buffers of the step live in the system, so the
+// captured pointers stay valid; per-call scratch inside the step becomes
+// graph allocation nodes.
+static bool use_step_graph(const pn_system *sys) {
+  const char *v = getenv("PN_GRAPH");
+  if (v) return strcmp(v, "0") != 0;
+  return (long long)sys->m * (sys->n + 1) <= 128LL * 129;
+}
+
+// Capture the device step once, after a direct step has sized every arena
+// and cached every table (so nothing inside allocates synchronously).  If
+// the runtime refuses any call under capture, the system keeps the direct
+// path (graph_state = -1); both paths launch the same kernels.
+template <class F>
+static void capture_step_graph(pn_system *sys, F &&device_step) {
+  sys->graph_state = -1;
+  if (!sys->graph_stream) {
+    if (cudaStreamCreateWithFlags(&sys->graph_stream, cudaStreamNonBlocking) != cudaSuccess) return;
+    for (auto &e : sys->gev)
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+  }
+  cudaStream_t gs = sys->graph_stream;
+  if (cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return;
+  const long long before = pn_launch_count();
+  bool ok = true;
+  try {
+    device_step(gs, sys->gev, true);
+  } catch (const Fail &) {
+    ok = false;
+  }
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(gs, &g);
+  sys->graph_launches = pn_launch_count() - before;
+  count_launch(-(int)sys->graph_launches);  // captured, not launched
+  if (ok && e == cudaSuccess && g) {
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+      sys->step_graph = exec;
+      sys->graph_state = 1;
+    }
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();  // a refused capture leaves no sticky error
+}
+
 extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, double *f, double *dx,
                               double *fmod, double *dxmod, double *xmod, pn_numinfo *info, void *stream) {
   PN_API_BEGIN
@@ -31,26 +78,41 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
   double *xa = sys->xbuf.d(), *A = sys->Abuf.d(), *fa = sys->fbuf.d();
   double *Q = sys->vbuf.d(), *R = sys->Rbuf.d(), *dxa = sys->xsol.d(), *xn = dxa + (size_t)n * es;
 
-  cudaEvent_t ev[5];
-  for (auto &e : ev) PN_CHECK_CUDA(cudaEventCreate(&e));
+  cudaEvent_t evl[5];
+  for (auto &e : evl) PN_CHECK_CUDA(cudaEventCreate(&e));
   struct EvGuard {
     cudaEvent_t *e;
     ~EvGuard() {
       for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
     }
-  } guard{ev};
+  } guard{evl};
+  // the device step from x (AoS in xa) to x_next; `external` records the
+  // phase events as graph nodes visible outside the graph
+  auto device_step = [&](cudaStream_t s, cudaEvent_t *e, bool external) {
+    auto rec = [&](cudaEvent_t ev) {
+      PN_CHECK_CUDA(external ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal) : cudaEventRecord(ev, s));
+    };
+    rec(e[0]);
+    // A = J(x) with b = -f(x) in column n (newton.py:84-87)
+    evaldiff_device(sys, xa, fa, A, m, n, s);
+    rec(e[1]);
+    mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, s);
+    rec(e[4]);
+    backsub_device(nc, cplx, n, R, dxa, sys->mgs, s);
+    rec(e[2]);
+    // x_next = x + dx (newton.py:92)
+    vec_op_aos(nc, cplx, PN_OP_ADD, n, xa, dxa, xn, s);
+    rec(e[3]);
+  };
   planes_to_aos(es, n, din.d, xa, st);
-  PN_CHECK_CUDA(cudaEventRecord(ev[0], st));
-  // A = J(x) with b = -f(x) in column n (newton.py:84-87)
-  evaldiff_device(sys, xa, fa, A, m, n, st);
-  PN_CHECK_CUDA(cudaEventRecord(ev[1], st));
-  mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, st);
-  PN_CHECK_CUDA(cudaEventRecord(ev[4], st));
-  backsub_device(nc, cplx, n, R, dxa, sys->mgs, st);
-  PN_CHECK_CUDA(cudaEventRecord(ev[2], st));
-  // x_next = x + dx (newton.py:92)
-  vec_op_aos(nc, cplx, PN_OP_ADD, n, xa, dxa, xn, st);
-  PN_CHECK_CUDA(cudaEventRecord(ev[3], st));
+  const bool graph = sys->graph_state == 1 && use_step_graph(sys);
+  cudaEvent_t *ev = graph ? sys->gev : evl;
+  if (graph) {
+    PN_CHECK_CUDA(cudaGraphLaunch(sys->step_graph, st));
+    count_launch((int)sys->graph_launches);
+  } else {
+    device_step(st, evl, false);
+  }
 
   DevOut o_x(x_next, (size_t)n * es, st), o_f(f, (size_t)m * es, st), o_dx(dx, (size_t)n * es, st);
   DevOut o_fm(fmod, (size_t)m * nc, st), o_dm(dxmod, (size_t)n * nc, st), o_xm(xmod, (size_t)n * nc, st);
@@ -95,6 +157,7 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
     info->t_factor = mf * 1e-3;
   }
   PN_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (sys->graph_state == 0 && use_step_graph(sys)) capture_step_graph(sys, device_step);
   PN_API_END
 }
 

@@ -37,6 +37,10 @@ pn_system::~pn_system() {
   cudaFree(fused.d_chunk_seg);
   cudaFree(fused.d_poly_chunk);
   if (ev) cudaEventDestroy(ev);
+  if (step_graph) cudaGraphExecDestroy(step_graph);
+  for (auto e : gev)
+    if (e) cudaEventDestroy(e);
+  if (graph_stream) cudaStreamDestroy(graph_stream);
 }
 
 namespace {

@@ -186,7 +186,7 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp", "pipe"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp", "pipe", "small"])
 def mgs_mode(request, monkeypatch):
     """Every MGS schedule (priority flow, dataflow, launch per sweep, warp per column)."""
     monkeypatch.setenv("PN_MGS_MODE", request.param)
