@@ -1547,7 +1547,8 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
   // qd keeps the dataflow kernel, whose 33 CTAs sweep the columns in
   // parallel: 1.07 vs 1.14 ms; PN_MGS_MODE=small forces it, larger m take
   // the default schedule)
-  if (m <= 32 && (mode == 5 || (!getenv("PN_MGS_MODE") && Traits<E>::nc <= 2))) {
+  const bool mode_set = getenv("PN_MGS_MODE") != nullptr;
+  if (m <= 32 && (mode == 5 || (!mode_set && Traits<E>::nc <= 2))) {
     const size_t smem = (size_t)Traits<E>::es * (n + 1) * 32 * sizeof(double);
     auto kern = k_mgs_small<E>;
     if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
