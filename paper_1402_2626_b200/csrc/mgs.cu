@@ -1455,8 +1455,8 @@ static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
 // warp sweeps its later columns, one barrier.  Sums over rows are the warp
 // shuffle tree with right pruning = tree_sum's order (mgs.py:145-221); no
 // inter-CTA flags, so a pivot costs its arithmetic chain plus two barriers.
-template <class E>
-__global__ void __launch_bounds__(512) k_mgs_small(const double *__restrict__ A, int m, int n, double eps,
+template <class E, int NT>
+__global__ void __launch_bounds__(NT) k_mgs_small(const double *__restrict__ A, int m, int n, double eps,
                                                    double *__restrict__ Q, double *__restrict__ R,
                                                    MgsStatus *status) {
   using Rl = typename Traits<E>::R;
@@ -1550,9 +1550,11 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
   const bool mode_set = getenv("PN_MGS_MODE") != nullptr;
   if (m <= 32 && (mode == 5 || (!mode_set && Traits<E>::nc <= 2))) {
     const size_t smem = (size_t)Traits<E>::es * (n + 1) * 32 * sizeof(double);
-    auto kern = k_mgs_small<E>;
+    // plain double: a warp per column (up to 32); dd/qd: 16 warps (registers)
+    constexpr int NT = Traits<E>::nc == 1 ? 1024 : 512;
+    auto kern = k_mgs_small<E, NT>;
     if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int nt = std::min(512, 32 * (n + 1));
+    const int nt = std::min(NT, 32 * (n + 1));
     kern<<<1, nt, smem, st>>>(A, m, n, eps, Q, R, status);
     PN_CHECK_LAUNCH();
     count_launch(1);
@@ -2094,15 +2096,14 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
     const int par = b & 1;
     if (blockIdx.x == 0) {
       const int ncu = (b > 0 && b + 1 < nb) ? min(n, lo + 64) - (lo + 32) : 0;
-      if (warp == 0) {
-        for (int jj = 0; jj < nbk; ++jj)
-          if (lane <= jj) sD[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo + lane) * es);
-        if (lane < nbk) sP[lane] = prep[lo + lane];
-      } else if (warp == 1 && b > 0) {
-        for (int jj = 0; jj < nbk; ++jj) sU[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + lane) * es);
-        for (int jj = 0; jj < ncu; ++jj)
-          sV[jj * 32 + lane] = eload<E>(R + ((long long)(lo + 32 + jj) * ld + lo - 32 + lane) * es);
+      // stage the blocks with every thread of the CTA, all loads independent
+      for (int e = threadIdx.x; e < 32 * 32; e += NT) {
+        const int jj = e >> 5, ii = e & 31;
+        if (jj < nbk && ii <= jj) sD[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo + ii) * es);
+        if (b > 0 && jj < nbk) sU[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + ii) * es);
+        if (jj < ncu) sV[e] = eload<E>(R + ((long long)(lo + 32 + jj) * ld + lo - 32 + ii) * es);
       }
+      if (threadIdx.x < nbk) sP[threadIdx.x] = prep[lo + threadIdx.x];
       __syncthreads();
       if (warp == 0) {
         E yr = ezero<E>();
