@@ -454,8 +454,8 @@ static void launch_fused(pn_system *sys, const double *x, const double *table, d
 // double buffered, so the next chunk's supports stream in while the current
 // chunk's trees compute and no lane waits on a dependent index load.  The
 // arithmetic is mono_tree_eval, identical to k_mono_tree.
-template <class E, int BASE, int G, int NT>
-__global__ void __launch_bounds__(NT) k_mono_tree_tma(const int32_t *__restrict__ list, long long count, int K,
+template <class E, int BASE, int G, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) k_mono_tree_tma(const int32_t *__restrict__ list, long long count, int K,
                                                       long long e0, const int32_t *__restrict__ var,
                                                       const int32_t *__restrict__ exps,
                                                       const int32_t *__restrict__ dst, const double *__restrict__ coeff,
@@ -715,6 +715,15 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
       while (KS % 32 != G % 32) ++KS;
     const size_t smem = (size_t)(6 * CH * KS + 2 * CH) * sizeof(int);
     auto kern = k_mono_tree_tma<E, BASE, G, NT>;
+    if constexpr (Traits<E>::nc >= 2 && BASE == 32) {
+      // register cap for occupancy: qd 3 CTAs per SM (168 registers, cqd
+      // eval 11.9 -> 11.3 ms), dd 4 (128 registers, C5 4190 -> 4260
+      // start-iterations/s); PN_TREE_MINB=1|3|4 overrides
+      const char *mb = getenv("PN_TREE_MINB");
+      const int minb = mb ? atoi(mb) : (Traits<E>::nc == 4 ? 3 : 4);
+      if (minb == 3) kern = k_mono_tree_tma<E, BASE, G, NT, 3>;
+      if (minb == 4) kern = k_mono_tree_tma<E, BASE, G, NT, 4>;
+    }
     if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
