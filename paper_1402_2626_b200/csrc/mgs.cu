@@ -1289,17 +1289,26 @@ static void trace_end(int n, unsigned long long *buf, cudaStream_t st) {
   }
 }
 
-// Column ownership of the flow kernel: CTA c owns one column of every round
-// of G consecutive columns.  "rr" (default): column c of each round (c, c+G,
-// ...), which keeps the number of unfinished columns per CTA within one of
-// each other at every point of the factorisation; "snake": the direction
-// alternates per round (c, 2G-1-c, 2G+c, ...).  Snake brings pivot n-C out
-// 14 ms sooner on the cqd step, but leaves the tail kernel's columns behind
-// and the launch ends 4 ms later (profiles/r01, trace of PN_MGS_TRACE).
-// PN_FLOW_OWN=rr|snake|<file> (file: one line per CTA, its columns).
+// Column ownership of the flow kernel.  A CTA applies its columns' sweeps
+// one at a time and shares its SM with one other CTA (c and c + S, S SMs),
+// so what has to be balanced is the sweep count per SM over time.
+// "smsnake" (default with two CTAs per SM): rounds of S columns are dealt to
+// the SMs in alternating direction (SM s gets s, 2S-1-s, 2S+s, ...), which
+// gives every SM the same total over the full rounds (max/mean 1.02 at
+// n = 1024 vs 1.13 for round robin), and an SM's columns alternate between
+// its two CTAs; cqd MGS 106.3 -> 102.9 ms.  "rr": CTA c owns c, c+G, ...;
+// "snake": CTA-level alternating direction (pivot n-C 14 ms sooner but the
+// tail kernel's columns are left behind: +4 ms).  Other in-SM splits
+// (greedy by load, ABBA) were slower (scripts/own/*.txt, profiles/r01).
+// PN_FLOW_OWN=smsnake|rr|snake|<file> (file: one line per CTA, its columns).
 static void flow_owner_table(int n, int G, MgsWork &w, cudaStream_t st) {
   const char *v = getenv("PN_FLOW_OWN");
-  const int var = !v || strcmp(v, "rr") == 0 ? 0 : strcmp(v, "snake") == 0 ? 1 : 2;
+  const int S = num_sms();
+  const bool pairs = G == 2 * S;  // two CTAs per SM: c and c + S share one
+  const int var = !v ? (pairs ? 3 : 0)
+                     : strcmp(v, "rr") == 0 ? 0
+                     : strcmp(v, "snake") == 0 ? 1
+                     : strcmp(v, "smsnake") == 0 ? (pairs ? 3 : 0) : 2;
   const long long key = ((long long)n << 32) | ((long long)G << 4) | var;
   if (w.own_key == key && var != 2) return;
   std::vector<std::vector<int>> lists(G);
@@ -1321,6 +1330,14 @@ static void flow_owner_table(int n, int G, MgsWork &w, cudaStream_t st) {
       }
     }
     fclose(fp);
+  } else if (var == 3) {
+    // SM-level snake: round r of S columns goes to SMs 0..S-1, alternating
+    // direction; an SM's r-th column goes to its CTA s (r even) or s + S
+    for (int j = 0; j <= n; ++j) {
+      const int r = j / S, i = j % S;
+      const int sm = (r & 1) ? S - 1 - i : i;
+      lists[sm + ((r & 1) ? S : 0)].push_back(j);
+    }
   } else {
     for (int j = 0; j <= n; ++j) {
       const int r = j / G, i = j % G;

@@ -1,7 +1,7 @@
 """The quad-double flow kernel's schedule knobs change only who applies which
 sweep when, never the operation sequence of a column (mgs.py:171-215): Q, R,
 x and z must stay bit-identical to the oracle under every column ownership
-(PN_FLOW_OWN=rr|snake|<table file>) and hold rule (PN_FLOW_HOLD), and a table
+(PN_FLOW_OWN=smsnake|rr|snake|<table file>) and hold rule (PN_FLOW_HOLD), and a table
 that leaves a column unowned is refused instead of stalling the pivots."""
 
 import os
@@ -57,7 +57,8 @@ def _check(res, ref):
 
 
 @pytest.mark.parametrize("own,hold,pick", [("rr", "0", "0"), ("rr", "3", "1"), ("snake", "1", "0"),
-                                           ("snake", "0", "1"), ("rr", "1", "0")])
+                                           ("snake", "0", "1"), ("rr", "1", "0"), ("smsnake", "1", "1"),
+                                           ("smsnake", "0", "0")])
 def test_flow_schedules_bit_identical(gpu, case, own, hold, pick):
     aug, ref = case
     with env(PN_MGS_MODE="flow", PN_FLOW_OWN=own, PN_FLOW_HOLD=hold, PN_FLOW_PICK=pick):
