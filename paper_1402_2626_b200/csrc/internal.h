@@ -122,6 +122,7 @@ struct MgsWork {
   DevArena status;  // MgsStatus
   DevArena ready;   // dataflow schedule: pivot-published flags (n+1 ints)
   DevArena own;     // flow schedule: column ownership table (G x maxo ints)
+  DevArena smslot;  // flow schedule: CTAs registered per SM id
   long long own_key = -1;
   int own_maxo = 0;
 };

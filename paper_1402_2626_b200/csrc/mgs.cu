@@ -461,7 +461,8 @@ template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
                                                     MgsStatus *status, int *ready, int kstop, int hold, int lag,
-                                                    const int *__restrict__ own, int maxo, int pickrule) {
+                                                    const int *__restrict__ own, int maxo, int pickrule,
+                                                    int *smslot, int S) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
@@ -478,11 +479,41 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
   const int lane = tid & 31, w = tid >> 5;
   const int row0 = tid * B;
   const int nparts = (m + B - 1) / B;
+  // Which table row this CTA takes.  With smslot, rows follow the SM the
+  // CTA actually runs on (row = dense SM rank + S * slot on that SM), so the
+  // SM-level schedule of the table holds whatever the block scheduler did;
+  // if the placement is not exactly two CTAs on each of S SMs, every CTA
+  // falls back to its block index (the same decision everywhere).
+  int row = cta;
+  if (smslot) {
+    __shared__ int s_row;
+    unsigned smid, nsm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    int slot = 0;
+    if (tid == 0) slot = atomicAdd(smslot + smid, 1);
+    cooperative_groups::this_grid().sync();
+    if (tid == 0) {
+      int rank = 0, used = 0;
+      bool even = true;
+      for (unsigned i = 0; i < nsm && i < 1024; ++i) {
+        const int c = ld_acquire(smslot + i);
+        if (c) {
+          ++used;
+          even &= c == 2;
+          if (i < smid) ++rank;
+        }
+      }
+      s_row = (even && used == S) ? rank + S * slot : cta;
+    }
+    __syncthreads();
+    row = s_row;
+  }
   // the CTA's columns, ascending (own: maxo per CTA, -1 padded)
   int cols[64];
   int nown = 0;
   for (int i = 0; i < maxo && i < 64; ++i) {
-    const int j = own[cta * maxo + i];
+    const int j = own[row * maxo + i];
     if (j < 0) break;
     cols[nown++] = j;
   }
@@ -1419,7 +1450,19 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   // cqd MGS 107.5 -> 106.8 ms), 0 = lowest index (earliest deadline)
   const char *pv = getenv("PN_FLOW_PICK");
   int pickrule = pv ? atoi(pv) : 1;
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule};
+  // PN_FLOW_SMMAP=1: table rows by the SM a CTA lands on instead of the
+  // block index (guards the SM pairing c / c + S the smsnake table assumes;
+  // measured 1 ms slower than the block-index rows, which already pair up)
+  const char *mv = getenv("PN_FLOW_SMMAP");
+  int *smslot = nullptr;
+  int nsms = num_sms();
+  if (grid == 2 * nsms && mv && strcmp(mv, "1") == 0) {
+    w.smslot.ensure(1024 * sizeof(int));
+    PN_CHECK_CUDA(cudaMemsetAsync(w.smslot.p, 0, 1024 * sizeof(int), st));
+    smslot = w.smslot.as<int>();
+  }
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule,
+                  &smslot, &nsms};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));

@@ -65,6 +65,13 @@ def test_flow_schedules_bit_identical(gpu, case, own, hold, pick):
         _check(_solve(aug), ref)
 
 
+def test_flow_rows_by_sm(gpu, case):
+    """PN_FLOW_SMMAP=1: table rows chosen by the SM each CTA runs on."""
+    aug, ref = case
+    with env(PN_MGS_MODE="flow", PN_FLOW_SMMAP="1"):
+        _check(_solve(aug), ref)
+
+
 def test_flow_table_file(gpu, case, tmp_path):
     """A shuffled ownership table (296 CTAs, columns dealt at random)."""
     aug, ref = case
