@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
 // pairwise order (the top levels), so r_kj, the norms and therefore Q and R
 // stay bit-identical.  Pivot j is published when all S parts have stored
 // their rows of q_j (ready[j] counts to S).
-template <class E, int B, int NT>
+template <class E, int B, int NT, bool CL = false>
 __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ A, int m, int n, const double *__restrict__ orig,
                                                  double eps, double *__restrict__ Q, double *__restrict__ R,
                                                  MgsStatus *status, int *ready, int kstop, int S,
@@ -773,9 +773,36 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
   // exchange slot of column ci: [2 parity][S] elements (E units) + flags
   E *xe = reinterpret_cast<E *>(xch) + (long long)ci * 2 * S;
   int *xf = xflag + (long long)ci * 2 * S;
+  // CL: the S parts of a column form a thread-block cluster and exchange
+  // through distributed shared memory: each part leaves its partial in its
+  // own shared slot (parity-double-buffered like the global slots), one
+  // cluster barrier, thread 0 reads the S slots of the cluster.  A slot is
+  // rewritten two exchanges later, after every peer has passed the barrier
+  // that follows its read.
+  __shared__ __align__(16) double s_xch[2][es];
+  auto cl_sync = [&]() {
+    if constexpr (CL) cooperative_groups::this_cluster().sync();
+  };
   // publish this part's partial with tag, gather all S, combine in tree order
   auto exchange = [&](auto v, int tag) {
     using T = decltype(v);
+    if constexpr (CL) {
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      T *mine = reinterpret_cast<T *>(s_xch[tag & 1]);
+      if (tid == 0) *mine = v;
+      cl.sync();
+      T acc = v;
+      if (tid == 0) {
+        T w[8];
+        for (int p = 0; p < sparts; ++p) w[p] = *cl.map_shared_rank(mine, p);
+        for (int st = 1; st < sparts; st <<= 1)
+          for (int p = 0; p + st < sparts; p += 2 * st) w[p] = eadd(w[p], w[p + st]);
+        acc = w[0];
+        s_ok = 1;
+      }
+      return acc;
+    }
     T *slot = reinterpret_cast<T *>(xe + (tag & 1) * S);
     if (tid == 0) {
       slot[part] = v;
@@ -823,7 +850,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
         s_ok = ok;
       }
       __syncthreads();
-      if (!s_ok) return;
+      if (!s_ok) {  // every part of a column waits on the same flag: all leave here
+        cl_sync();
+        return;
+      }
       const double *qk = Q + (long long)k * m * es;
       E qv[B];
 #pragma unroll
@@ -864,6 +894,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
           __threadfence();
           atomicExch(&status->code, PN_E_BREAKDOWN);
         }
+        cl_sync();  // the peers may still read this CTA's exchange slot
         return;
       }
     }
@@ -879,6 +910,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
       if (tid == 0) atomicAdd(ready + j, 1);
     }
   }
+  cl_sync();  // keep the exchange slots alive until every peer has read them
 }
 
 // ---------------------------------------------------------------------------
@@ -1429,6 +1461,25 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
     int tper = 0;
     PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, tk, tnt, 0));
     C = std::min(n + 1, tper * num_sms() / S);
+    const char *cv0 = getenv("PN_MGS_TAIL_CLUSTER");
+    if (cv0 && strcmp(cv0, "1") == 0 && var == 'a') {
+      // clusters of S CTAs must fit inside a GPC: fewer columns co-reside
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(S);
+      cfg.blockDim = dim3(tnt);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)k_mgs_tail<E, 2, 128, true>, &cfg) == cudaSuccess)
+        C = std::min(C, ncl);
+      else
+        cudaGetLastError();
+    }
     if (tv && atoi(tv) > 0) C = std::min(C, atoi(tv));
     if (C >= 16) kstop = n + 1 - C;
     else C = 0;
@@ -1474,7 +1525,34 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
     double *xp = xch.d();
     int *xf = xfl.as<int>();
     void *targs[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &S, &xp, &xf};
-    PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, tnt, targs, 0, st));
+    // PN_MGS_TAIL_CLUSTER=1: the S parts of a column as one thread-block
+    // cluster exchanging through distributed shared memory (variant a)
+    const char *cv = getenv("PN_MGS_TAIL_CLUSTER");
+    bool launched = false;
+    if (cv && strcmp(cv, "1") == 0 && var == 'a') {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C * S);
+      cfg.blockDim = dim3(tnt);
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = S;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      const cudaError_t le = cudaLaunchKernelExC(&cfg, (const void *)k_mgs_tail<E, 2, 128, true>, targs);
+      launched = le == cudaSuccess;
+      if (!launched) {
+        cudaGetLastError();
+        static bool told = false;
+        if (!told) fprintf(stderr, "k_mgs_tail cluster launch refused (%s); plain launch\n", cudaGetErrorName(le));
+        told = true;
+      }
+    }
+    if (!launched) PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, tnt, targs, 0, st));
     count_launch(1);
   }
   trace_end(n, tr, st);
