@@ -187,12 +187,17 @@ int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, double *f, voi
 /* ---- synthetic inputs -------------------------------------------------------- */
 /* SURVEY 8(d) F(n, T, k, seed, maxexp, m): m polynomials in n variables, T
  * monomials each of k distinct variables (uniform subset), exponents uniform
- * in [1, maxexp], coefficient parts uniform in +-[0.5, 2).  Outputs CSR in
- * generation order plus binary64 coefficients coef_re/coef_im (M each;
- * coef_im may be NULL for real systems).  Arrays must be preallocated:
- * poly_ptr[m+1], mon_ptr[m*T+1], var_idx/exps[m*T*k]. */
-int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t k, int32_t maxexp, uint64_t seed,
-                              int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx, int32_t *exps,
+ * in [1, maxexp], coefficient parts uniform in +-[0.5, 2).  kmin < k gives
+ * the C2 "mixed" variant: each monomial's variable count is uniform in
+ * [kmin, k] (kmin == k draws nothing extra, so the uniform family is
+ * unchanged).  Outputs CSR in generation order plus binary64 coefficients
+ * coef_re/coef_im (M each; coef_im may be NULL for real systems).  Arrays
+ * must be preallocated: poly_ptr[m+1], mon_ptr[m*T+1], var_idx/exps[m*T*k]
+ * (the actual entry count is mon_ptr[m*T]).  The oracle carries an
+ * independent restatement (or_generate_random_system) that the reference
+ * arm of bench.py uses, so that arm never loads this library. */
+int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t kmin, int32_t k, int32_t maxexp,
+                              uint64_t seed, int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx, int32_t *exps,
                               double *coef_re, double *coef_im);
 
 #ifdef __cplusplus

@@ -44,6 +44,7 @@ def lib():
         L.or_back_substitute.argtypes = [i, i, i, vp, vp, vp]
         L.or_least_squares.argtypes = [i, i, i, i, vp, vp, vp, vp, vp, vp, i]
         L.or_newton_step.argtypes = [i, i, i, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i]
+        L.or_generate_random_system.argtypes = [i, i, i, i, i, i, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -180,6 +181,35 @@ class CSR:
         cat = (lambda xs: np.concatenate(xs).astype(np.int32)) if vi else (lambda xs: np.zeros(0, np.int32))
         return CSR(self.n_vars, np.asarray(pp, np.int32), np.asarray(mp, np.int32), cat(vi), cat(ex),
                    np.ascontiguousarray(self.coeffs[..., cols]))
+
+
+def random_sparse_csr(n: int, T: int, k: int, level: Level, seed: int, maxexp: int = 1, m=None,
+                      kmin=None) -> CSR:
+    """F(n, T, k, level, seed, maxexp, m[, kmin]) from the
+    oracle's own generator (or_generate_random_system), in generation order;
+    coefficients as level.from_float(re, im) planes.  Same arrays as the
+    product's random_sparse_system, without loading the product library."""
+    m = n if m is None else m
+    kmin = k if kmin is None else kmin
+    M = m * T
+    poly_ptr = np.empty(m + 1, np.int32)
+    mon_ptr = np.empty(M + 1, np.int32)
+    var_idx = np.empty(M * k, np.int32)
+    exps = np.empty(M * k, np.int32)
+    re = np.empty(M)
+    im = np.empty(M) if level.cplx else None
+    rc = lib().or_generate_random_system(m, n, T, kmin, k, maxexp, seed, _p(poly_ptr), _p(mon_ptr), _p(var_idx),
+                                         _p(exps), _p(re), _p(im))
+    if rc:
+        raise ValueError("or_generate_random_system: bad arguments")
+    nnz = int(mon_ptr[M])
+    coeffs = np.zeros(level.cshape + (M,))
+    if level.cplx:
+        coeffs[0, 0] = re + 0.0
+        coeffs[1, 0] = im + 0.0
+    else:
+        coeffs[0] = re + 0.0
+    return CSR(n, poly_ptr, mon_ptr, var_idx[:nnz].copy(), exps[:nnz].copy(), coeffs)
 
 
 # -- entry points ----------------------------------------------------------------

@@ -801,4 +801,64 @@ int or_newton_step(int nc, int cplx, int m, int n, const int *poly_ptr, const in
     return rc;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Synthetic input family F(n, T, k, seed, maxexp, m[, kmin]).
+ * The reference has no random sparse generator (its bench.py:98-110 only
+ * builds full-product stress monomials); this is an independent C
+ * restatement of the builder-defined family so that bench.py's
+ * --impl reference arm builds its inputs without loading the product
+ * library.  splitmix64 stream, Floyd's k-subset, sorted variables, exponents
+ * 1 + below(maxexp), coefficient parts (0.5 + 1.5 u) with a random sign.
+ * kmin < k: the variable count is drawn first, uniform in [kmin, k].
+ * tests/test_host.py checks it array-for-array against the product's
+ * pn_generate_random_system. */
+static uint64_t sm_state;
+static uint64_t sm_next(void) {
+    uint64_t z = (sm_state += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint32_t sm_below(uint32_t bound) { return (uint32_t)(((unsigned __int128)sm_next() * bound) >> 64); }
+static double sm_uniform(void) { return (double)(sm_next() >> 11) * 0x1.0p-53; }
+
+int or_generate_random_system(int m, int n, int T, int kmin, int k, int maxexp, uint64_t seed, int *poly_ptr,
+                              int *mon_ptr, int *var_idx, int *exps, double *coef_re, double *coef_im) {
+    if (m < 0 || n < 1 || T < 0 || kmin < 0 || kmin > k || k > n || maxexp < 1) return -1;
+    sm_state = seed * 0x2545F4914F6CDD1Dull + 0x1234567ull;
+    int *pick = (int *)malloc(sizeof(int) * (k > 0 ? k : 1));
+    long mon = 0, ent = 0;
+    poly_ptr[0] = 0;
+    mon_ptr[0] = 0;
+    for (int i = 0; i < m; ++i) {
+        for (int t = 0; t < T; ++t) {
+            int kt = kmin < k ? kmin + (int)sm_below((uint32_t)(k - kmin + 1)) : k;
+            int cnt = 0;
+            for (int j = n - kt; j < n; ++j) {
+                int r = (int)sm_below((uint32_t)j + 1), seen = 0;
+                for (int q = 0; q < cnt; ++q) seen |= pick[q] == r;
+                /* insertion keeps pick sorted */
+                int v = seen ? j : r, q = cnt++;
+                while (q > 0 && pick[q - 1] > v) { pick[q] = pick[q - 1]; --q; }
+                pick[q] = v;
+            }
+            for (int q = 0; q < cnt; ++q) {
+                var_idx[ent] = pick[q];
+                exps[ent] = 1 + (int)sm_below((uint32_t)maxexp);
+                ++ent;
+            }
+            double re = 0.5 + 1.5 * sm_uniform();
+            if (sm_next() & 1) re = -re;
+            double im = 0.5 + 1.5 * sm_uniform();
+            if (sm_next() & 1) im = -im;
+            coef_re[mon] = re;
+            if (coef_im) coef_im[mon] = im;
+            mon_ptr[++mon] = (int)ent;
+        }
+        poly_ptr[i + 1] = (int)mon;
+    }
+    free(pick);
+    return 0;
+}
+
 int or_version(void) { return 1; }

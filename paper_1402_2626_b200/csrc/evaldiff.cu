@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
                                                    const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                                                    const double *__restrict__ x, const double *__restrict__ table,
                                                    const int32_t *__restrict__ toff, double *__restrict__ contrib,
-                                                   BView bv) {
+                                                   BView bv, double *__restrict__ gscratch, long long gstride) {
   constexpr int es = Traits<E>::es;
   {
     const long long b = bslot(bv);
@@ -560,7 +560,11 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
     contrib += b * bv.c;
   }
   extern __shared__ __align__(16) double smem[];
-  E *lvl = reinterpret_cast<E *>(smem);  // levels back to back: 2*BASE entries
+  // levels back to back (2*base entries) then base complements; in shared
+  // memory when 3*base elements fit, otherwise in a per-CTA slice of global
+  // scratch (L2 resident: 3*base*es*8 bytes per CTA), so k is bounded by n only
+  E *lvl = gscratch ? reinterpret_cast<E *>(gscratch + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * gstride)
+                    : reinterpret_cast<E *>(smem);
   __shared__ E s_scale;
   for (long long g = blockIdx.x; g < count; g += gridDim.x) {
     const int c = list[g];
@@ -819,16 +823,22 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
     } else {
       int base = 1;
       while (base * 2 <= sys->max_k) base *= 2;
-      const size_t smem = (size_t)3 * base * es * sizeof(double);
-      PN_REQUIRE(smem <= 227 * 1024, PN_E_ARG,
-                 "monomials with %d variables exceed the shared-memory tree capacity", sys->max_k);
+      size_t smem = (size_t)3 * base * es * sizeof(double);
       constexpr int NT = 256;
-      PN_CHECK_CUDA(cudaFuncSetAttribute(k_mono_large<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
       const int gx = (int)std::min<long long>(b.count, std::max(1LL, (long long)num_sms() * 8 / nb));
+      double *gscratch = nullptr;
+      const long long gstride = 3LL * base * es;
+      if (smem > 227 * 1024) {  // levels in global memory (see k_mono_large)
+        sys->tree_scratch.ensure((size_t)gx * nb * gstride * sizeof(double));
+        gscratch = sys->tree_scratch.d();
+        smem = 0;
+      } else {
+        PN_CHECK_CUDA(cudaFuncSetAttribute(k_mono_large<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+      }
       k_mono_large<E, NT><<<dim3(gx, nb), NT, smem, st>>>(b.d_list, b.count, sys->d_mon_ptr, sys->d_var,
                                                           sys->d_exp, sys->d_dst, sys->d_coeff, x, table,
-                                                          sys->d_toff, contrib, bv);
+                                                          sys->d_toff, contrib, bv, gscratch, gstride);
       PN_CHECK_LAUNCH();
       count_launch(1);
     }

@@ -189,6 +189,7 @@ struct pn_system {
   // scratch reused across evaluations
   pn::DevArena contrib;  // (M + nnz) * es
   pn::DevArena table;    // table_len * es
+  pn::DevArena tree_scratch;  // k_mono_large levels when 3*base elements exceed shared memory
   pn::DevArena xbuf;     // n * es
   pn::DevArena Abuf;     // m * (n+1) * es (Newton / evaldiff output)
   pn::DevArena Rbuf, xsol, fbuf, vbuf;

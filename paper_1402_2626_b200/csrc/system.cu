@@ -410,12 +410,12 @@ struct SplitMix {
 };
 }  // namespace
 
-extern "C" int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t k, int32_t maxexp, uint64_t seed,
-                                         int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx, int32_t *exps,
-                                         double *coef_re, double *coef_im) {
+extern "C" int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t kmin, int32_t k, int32_t maxexp,
+                                         uint64_t seed, int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx,
+                                         int32_t *exps, double *coef_re, double *coef_im) {
   PN_API_BEGIN
-  PN_REQUIRE(m >= 0 && n >= 1 && T >= 0 && k >= 0 && k <= n && maxexp >= 1, PN_E_ARG,
-             "pn_generate_random_system: need 0 <= k <= n, maxexp >= 1");
+  PN_REQUIRE(m >= 0 && n >= 1 && T >= 0 && kmin >= 0 && kmin <= k && k <= n && maxexp >= 1, PN_E_ARG,
+             "pn_generate_random_system: need 0 <= kmin <= k <= n, maxexp >= 1");
   PN_REQUIRE((int64_t)m * T * k < (int64_t)1 << 31, PN_E_ARG, "pn_generate_random_system: too many terms");
   SplitMix rng{seed * 0x2545F4914F6CDD1Dull + 0x1234567ull};
   std::vector<int32_t> pick(k);
@@ -424,9 +424,12 @@ extern "C" int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_
   mon_ptr[0] = 0;
   for (int32_t i = 0; i < m; ++i) {
     for (int32_t t = 0; t < T; ++t) {
-      // Floyd's algorithm: k distinct values of [0, n)
+      // "mixed" variant: k_t uniform in [kmin, k]; no draw when kmin == k, so
+      // the uniform family's stream is unchanged
+      const int32_t kt = kmin < k ? kmin + (int32_t)rng.below((uint32_t)(k - kmin + 1)) : k;
+      // Floyd's algorithm: kt distinct values of [0, n)
       int cnt = 0;
-      for (int32_t j = n - k; j < n; ++j) {
+      for (int32_t j = n - kt; j < n; ++j) {
         int32_t r = (int32_t)rng.below((uint32_t)j + 1);
         bool seen = false;
         for (int q = 0; q < cnt; ++q)

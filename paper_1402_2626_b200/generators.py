@@ -20,12 +20,15 @@ from .xprec import PrecisionLevel
 
 
 def random_sparse_system(n: int, T: int, k: int, level: PrecisionLevel, seed: int, maxexp: int = 1,
-                         m: int | None = None) -> PackedSystem:
+                         m: int | None = None, kmin: int | None = None) -> PackedSystem:
     """F(n, T, k, level, seed, maxexp, m): m polynomials of T monomials, each
     a product of k distinct variables with exponents in [1, maxexp] and
-    coefficient parts in +-[0.5, 2).  Built by the C ABI's
-    splitmix64 generator in generation order (not canonical)."""
+    coefficient parts in +-[0.5, 2).  ``kmin`` < k gives the C2
+    "mixed" variant (variable count per monomial uniform in [kmin, k]).
+    Built by the C ABI's splitmix64 generator in generation order (not
+    canonical)."""
     m = n if m is None else m
+    kmin = k if kmin is None else kmin
     M = m * T
     nnz = M * k
     poly_ptr = np.empty(m + 1, np.int32)
@@ -34,9 +37,13 @@ def random_sparse_system(n: int, T: int, k: int, level: PrecisionLevel, seed: in
     exps = np.empty(nnz, np.int32)
     re = np.empty(M)
     im = np.empty(M) if level.cplx else None
-    rc = _lib.load().pn_generate_random_system(m, n, T, k, maxexp, seed, _lib.ptr(poly_ptr), _lib.ptr(mon_ptr),
-                                               _lib.ptr(var_idx), _lib.ptr(exps), _lib.ptr(re), _lib.ptr(im))
+    rc = _lib.load().pn_generate_random_system(m, n, T, kmin, k, maxexp, seed, _lib.ptr(poly_ptr),
+                                               _lib.ptr(mon_ptr), _lib.ptr(var_idx), _lib.ptr(exps), _lib.ptr(re),
+                                               _lib.ptr(im))
     _lib.check(rc)
+    if kmin < k:
+        var_idx = var_idx[:mon_ptr[M]].copy()
+        exps = exps[:mon_ptr[M]].copy()
     coeffs = np.zeros(level.cshape + (M,))
     # level.from_float(v): DoubleDouble(v) = (v + 0.0, 0.0); QuadDouble alike
     if level.cplx:

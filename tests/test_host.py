@@ -92,6 +92,29 @@ def test_generator_is_deterministic_and_valid():
     assert np.all(a.coeffs[:, 1] == 0.0)
 
 
+@pytest.mark.parametrize("n,T,k,maxexp,m,kmin,lv", [
+    (64, 16, 8, 3, None, None, "cdd"), (1024, 64, 32, 3, None, 1, "cqd"), (50, 7, 5, 2, 80, 0, "rd"),
+    (1024, 8, 32, 1, 1536, None, "cqd")])
+def test_oracle_generator_matches_product_generator(n, T, k, maxexp, m, kmin, lv):
+    """bench.py's reference arm builds F(n,T,k) with the oracle's own
+    generator (no product library); it must give the product's arrays,
+    including the C2 "mixed" variant (kmin < k)."""
+    import oracle
+    from conftest import level_from_name, oracle_level
+    from paper_1402_2626_b200.generators import random_sparse_system
+    p = random_sparse_system(n, T, k, level_from_name(lv), seed=5, maxexp=maxexp, m=m, kmin=kmin)
+    c = oracle.random_sparse_csr(n, T, k, oracle_level(lv), seed=5, maxexp=maxexp, m=m, kmin=kmin)
+    for a, b in [(p.poly_ptr, c.poly_ptr), (p.mon_ptr, c.mon_ptr), (p.var_idx, c.var_idx), (p.exps, c.exps),
+                 (p.coeffs, c.coeffs)]:
+        assert np.array_equal(a, b)
+    ks = np.diff(c.mon_ptr)
+    lo = k if kmin is None else kmin
+    assert ks.min() >= lo and ks.max() <= k
+    if kmin is not None and T * (m or n) > 1000:
+        assert ks.min() == lo and ks.max() == k  # the whole range is drawn
+    assert c.exps.min() >= 1 and c.exps.max() <= maxexp
+
+
 def test_canonical_sparse_key_equals_dense_key():
     # SURVEY P5: the sparse key orders like the dense exponent vector
     from paper_1402_2626_b200.polyrep import Monomial
