@@ -99,3 +99,50 @@ def test_criterion5_mgs_qr_accuracy(gpu, base, resid, ortho):
                     np.ascontiguousarray(np.broadcast_to(f.Q[..., :, None, :], ctx.cshape + (m, n, n))))
     gram = ctx.float_approx(ctx.tree_sum(outer, axis=0))
     assert f"{float(np.max(np.abs(gram - np.eye(n)))):.1e}" == ortho
+
+
+def test_criterion9_structure_checks(gpu):
+    """Criterion 9 (test_acceptance.py:259-287): cyclic monomial counts
+    n^2 - n + 2 for n = 2..64, and Jacobians of Chandrasekhar n = 32 and
+    cyclic-12 (real double) equal binary64 central differences at 1e-6, all
+    evaluated by the GPU path."""
+    from paper_1402_2626_b200.evaldiff import evaluate_system
+    from paper_1402_2626_b200.generators import (chandrasekhar_system, cyclic_n_roots, cyclic_packed,
+                                                 random_point)
+    cdd = level_from_name("cdd")
+    D = level_from_name("rd")
+    for n in range(2, 65):
+        assert cyclic_n_roots(n, cdd).monomial_count() == n * n - n + 2
+        assert cyclic_packed(n, cdd).monomials == n * n - n + 2
+    h = 2.0 ** -26
+    for system, point in [(chandrasekhar_system(32, D), random_point(32, 5, D)),
+                          (cyclic_n_roots(12, D), random_point(12, 6, D))]:
+        n = system.n_vars
+        ev = evaluate_system(system, point)
+        J = np.asarray(ev.jacobian, dtype=np.float64)
+        # every +-h perturbation of every variable in one batched evaluation
+        X = np.repeat(np.asarray(point, np.float64)[None, :], 2 * n, axis=0)
+        X[np.arange(n), np.arange(n)] += h
+        X[n + np.arange(n), np.arange(n)] -= h
+        from paper_1402_2626_b200.batch import evaluate_batch
+        from paper_1402_2626_b200.evaldiff import PreparedSystem
+        F = evaluate_batch(PreparedSystem(system), X[None])[0]          # (2n, m)
+        want = ((F[:n] - F[n:]) / (2.0 * h)).T                            # (m, n)
+        assert np.all(np.abs(J - want) <= 1e-6 * (np.abs(want) + 1.0))
+
+
+@pytest.mark.parametrize("lv", ["cdd", "rqd", "cd"])
+def test_chandrasekhar_packed_equals_object_builder(gpu, lv):
+    """The numpy CSR builder of the H-equation (paper scale) equals
+    PackedSystem.from_system of the Monomial builder, component for
+    component (weights and -(c w) formed on the GPU in both)."""
+    from paper_1402_2626_b200.generators import chandrasekhar_packed, chandrasekhar_system
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    level = level_from_name(lv)
+    for n in (1, 2, 7, 33):
+        a = chandrasekhar_packed(n, level)
+        b = PackedSystem.from_system(chandrasekhar_system(n, level), level)
+        for x, y in ((a.poly_ptr, b.poly_ptr), (a.mon_ptr, b.mon_ptr), (a.var_idx, b.var_idx), (a.exps, b.exps)):
+            assert np.array_equal(x, y)
+        assert np.array_equal(a.coeffs, b.coeffs)
+        assert np.array_equal(np.signbit(a.coeffs), np.signbit(b.coeffs))

@@ -1,7 +1,8 @@
 """bench.py's reference arm (`--impl reference`) runs the oracle port on the
 host only, so its JSON line can be checked here without a GPU: the keys the
-driver reads, the reference-arm extras, and the same metric/config as our
-arm (bench.py contract)."""
+driver reads, the reference-arm extras, whole measured steps, the identical
+config dict as our arm, and that the arm never maps the product library
+(bench.py contract)."""
 
 import json
 import os
@@ -10,14 +11,31 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
+ARGV = ["--impl", "reference", "--dim", "48", "--terms", "24", "--k", "6", "--base", "dd", "--steps", "2",
+        "--warmup", "1", "--cpu-budget", "1"]
+
+PROBE = """
+import runpy, sys, json
+sys.argv = ["bench.py"] + json.loads(sys.argv[1])
+runpy.run_path("bench.py", run_name="__main__")
+maps = open("/proc/self/maps").read()
+print("PRODUCT_LIB_MAPPED=" + str("libpolynewt_b200" in maps))
+print("ORACLE_LIB_MAPPED=" + str("libpn_oracle" in maps))
+"""
+
+
+def _run_reference():
+    out = subprocess.run([sys.executable, "-c", PROBE, json.dumps(ARGV)], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env={**os.environ, "RANK": "0", "WORLD_SIZE": "1",
+                                                     "LOCAL_RANK": "0"})
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = out.stdout.strip().splitlines()
+    d = json.loads([ln for ln in lines if ln.startswith("{")][-1])
+    return d, lines
+
 
 def test_reference_arm_json_line():
-    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--dim", "48", "--terms", "24",
-           "--k", "6", "--base", "dd", "--steps", "1", "--warmup", "0", "--cpu-budget", "1"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                         env={**os.environ, "RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"})
-    assert out.returncode == 0, out.stderr[-2000:]
-    d = json.loads(out.stdout.strip().splitlines()[-1])
+    d, lines = _run_reference()
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
         assert key in d, key
@@ -26,4 +44,37 @@ def test_reference_arm_json_line():
     assert d["value"] > 0 and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
-    assert d["config"]["workload"].startswith("F(48,24,6) complex dd")
+    assert d["cpu_baseline"]["single_core"]["cores"] == 1
+    # whole steps, measured: the reported mean is the mean of the timed steps
+    assert d["steps"] == 2 and len(d["step_seconds"]) == 2
+    assert abs(d["ms_per_step"] - 1e3 * sum(d["step_seconds"]) / 2) < 1e-6
+    assert "extrapolated" not in d["cpu_baseline"]["sample"]
+    # no product library in the reference arm; the oracle is what runs
+    assert "PRODUCT_LIB_MAPPED=False" in lines
+    assert "ORACLE_LIB_MAPPED=True" in lines
+
+
+def test_reference_arm_config_equals_ours():
+    sys.path.insert(0, ROOT)
+    import bench
+    d, _ = _run_reference()
+    ours = bench.step_config(bench.parse(ARGV[2:]), 1)
+    assert d["config"] == ours
+    assert d["config"]["workload"].startswith("F(48,24,6) complex dd Newton step 48x48")
+
+
+def test_oracle_generator_matches_product_generator():
+    """The reference arm's inputs (oracle generator) equal our arm's (the
+    product's C generator), array for array."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle
+    from paper_1402_2626_b200.generators import random_sparse_system
+    from paper_1402_2626_b200.xprec import precision_level
+    for base, kmin, maxexp in (("qd", None, 1), ("dd", 1, 3)):
+        p = random_sparse_system(40, 17, 6, precision_level(base, True), seed=5, maxexp=maxexp, m=45, kmin=kmin)
+        c = oracle.random_sparse_csr(40, 17, 6, oracle.Level(base, True), seed=5, maxexp=maxexp, m=45, kmin=kmin)
+        for a, b in ((p.poly_ptr, c.poly_ptr), (p.mon_ptr, c.mon_ptr), (p.var_idx, c.var_idx), (p.exps, c.exps),
+                     (p.coeffs, c.coeffs)):
+            assert np.array_equal(np.asarray(a), np.asarray(b))

@@ -227,3 +227,21 @@ def test_with_constant_terms_host_logic():
         assert np.array_equal(q.var_idx, p.var_idx)
         kept = ks_q[ks_q > 0]
         assert np.array_equal(kept, np.diff(p.mon_ptr)[np.diff(p.mon_ptr) > 0])
+
+
+def test_cyclic_packed_equals_object_builder():
+    """The numpy CSR builder of cyclic n-roots (67 M support entries at
+    n = 512) equals PackedSystem.from_system of the Monomial builder."""
+    import numpy as np
+    from paper_1402_2626_b200.generators import cyclic_n_roots, cyclic_packed
+    from paper_1402_2626_b200.polyrep import PackedSystem
+    from paper_1402_2626_b200.xprec import precision_level
+    for base, cplx in (("dd", True), ("qd", False), ("d", True)):
+        level = precision_level(base, cplx)
+        for n in (2, 3, 8, 17):
+            a = cyclic_packed(n, level)
+            b = PackedSystem.from_system(cyclic_n_roots(n, level), level)
+            for x, y in ((a.poly_ptr, b.poly_ptr), (a.mon_ptr, b.mon_ptr), (a.var_idx, b.var_idx),
+                         (a.exps, b.exps), (a.coeffs, b.coeffs)):
+                assert np.array_equal(x, y)
+            assert np.array_equal(np.signbit(a.coeffs), np.signbit(b.coeffs))
