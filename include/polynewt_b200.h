@@ -130,6 +130,15 @@ int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t M, int64_t 
                      pn_system **out);
 int pn_system_destroy(pn_system *sys);
 int pn_system_get_stats(const pn_system *sys, pn_system_stats *stats);
+/* the evaluation plan chosen for the system (diagnostics and tests):
+ * rows_ok = 1 when the row kernel (k_eval_rows) can serve it, with its
+ * uniform monomial size K, monomials per chunk, per-variable stack depth and
+ * number of chunks */
+typedef struct {
+  int32_t rows_ok, K, chunk, depth;
+  int64_t nchunks;
+} pn_plan_info;
+int pn_system_plan_info(const pn_system *sys, pn_plan_info *info);
 /* canonical position -> input monomial index (M entries) */
 int pn_system_canonical_order(const pn_system *sys, int64_t *perm);
 /* analytic OpCounter of one evaluation (equals the reference's tallies) */

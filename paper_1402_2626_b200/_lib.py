@@ -50,6 +50,11 @@ class SystemStats(ctypes.Structure):
                 ("table_mul_ops", ctypes.c_int64), ("max_k", ctypes.c_int32), ("max_deg", ctypes.c_int32)]
 
 
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("rows_ok", ctypes.c_int32), ("K", ctypes.c_int32), ("chunk", ctypes.c_int32),
+                ("depth", ctypes.c_int32), ("nchunks", ctypes.c_int64)]
+
+
 # exported symbols and their signatures (argtypes, restype)
 SIGNATURES = {
     "pn_version": ([], ctypes.c_int),
@@ -66,6 +71,7 @@ SIGNATURES = {
                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "pn_system_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "pn_system_get_stats": ([ctypes.c_void_p, ctypes.POINTER(SystemStats)], ctypes.c_int),
+    "pn_system_plan_info": ([ctypes.c_void_p, ctypes.POINTER(PlanInfo)], ctypes.c_int),
     "pn_system_canonical_order": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "pn_system_counts": ([ctypes.c_void_p, ctypes.POINTER(Counts)], ctypes.c_int),
     "pn_evaldiff": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Counts),

@@ -23,6 +23,7 @@
 //   K2 k_segments    : one thread per output entry; a binary-counter fold of
 //                      the entry's contributions reproduces tree_sum's
 //                      right-pruned pairwise order exactly.
+#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cstring>
 
@@ -97,7 +98,13 @@ __global__ void k_mono_small(const int32_t *__restrict__ list, long long count, 
 
 // scale = coeff [* common]; common = left fold of x_v^(d-1) over d >= 2
 // (polyrep.py:133-139, evaldiff.py:168)
-template <class E>
+// support entries: plain (PK = 0: variable / exponent arrays) or packed
+// (PK = 1, k_eval_rows: var | chunk slot << 16 | exponent << 28)
+template <int PK> __device__ __forceinline__ int ent_var(int e) { return PK ? (e & 0xffff) : e; }
+template <int PK> __device__ __forceinline__ int ent_exp(int e) { return PK ? (int)((unsigned)e >> 28) : e; }
+template <int PK> __device__ __forceinline__ int ent_slot(int e) { return PK ? (int)(((unsigned)e >> 16) & 0xfff) : e; }
+
+template <class E, int PK = 0>
 __device__ __forceinline__ E monomial_scale(const E &co, int lo, int k, const int32_t *__restrict__ var,
                                             const int32_t *__restrict__ exps, const double *__restrict__ table,
                                             const int32_t *__restrict__ toff) {
@@ -105,9 +112,9 @@ __device__ __forceinline__ E monomial_scale(const E &co, int lo, int k, const in
   bool have = false;
   E common;
   for (int p = 0; p < k; ++p) {
-    const int d = exps[lo + p];
+    const int d = ent_exp<PK>(exps[lo + p]);
     if (d < 2) continue;
-    const E pw = eload<E>(table + ((long long)toff[var[lo + p]] + d - 2) * es);
+    const E pw = eload<E>(table + ((long long)toff[ent_var<PK>(var[lo + p])] + d - 2) * es);
     common = have ? emul(common, pw) : pw;
     have = true;
   }
@@ -126,7 +133,7 @@ template <> struct Log2<1> { static constexpr int value = 0; };
 // Results go through two sinks: value(v) on lane 0 of the group and
 // deriv(t, v) for every support position t of the monomial.  Inactive
 // groups (active == false) run the shuffles but emit nothing.
-template <class E, int BASE, int G, class VSink, class DSink>
+template <class E, int BASE, int G, int PK = 0, bool XSM = false, class VSink, class DSink>
 __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const int32_t *mv, const int32_t *me,
                                                const E &co, const double *__restrict__ x,
                                                const double *__restrict__ table, const int32_t *__restrict__ toff,
@@ -139,7 +146,12 @@ __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const 
   static_assert(BASE >= G && G >= 2 && G <= 32, "bad tree config");
   const int ell = k - BASE;
 
-  auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
+  // PK: mv / me hold packed entries (ent_var / ent_exp); XSM: x is in shared memory
+  auto leaf = [&](int t) -> E {
+    const double *p = x + (long long)ent_var<PK>(mv[t]) * es;
+    if constexpr (XSM) return eload<E>(p);
+    else return eload_ldg<E>(p);
+  };
   // slot t of level 0: v[t] * v[BASE+t] for t < ell, else v[t] (evaldiff.py:63-65)
   auto slot = [&](int t) -> E {
     E v = leaf(t);
@@ -178,7 +190,7 @@ __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const 
   // ---- value (evaldiff.py:166-172) ---------------------------------------
   // unit: every exponent is 1 (the bucket was checked on upload), so the
   // common factor is empty and scale == co
-  const E scale = unit ? co : monomial_scale<E>(co, 0, k, mv, me, table, toff);
+  const E scale = unit ? co : monomial_scale<E, PK>(co, 0, k, mv, me, table, toff);
   if (active && r == 0) value_sink(emul(scale, root));
 
   // ---- downward sweep of complements (evaldiff.py:89-98) -----------------
@@ -226,13 +238,13 @@ __device__ __forceinline__ void mono_tree_eval(int r, bool active, int k, const 
       const int t2 = BASE + t;
       const E g1 = emul(cl[u], leaf(t2));
       const E g2 = emul(cl[u], leaf(t));
-      const int d1 = unit ? 1 : me[t], d2 = unit ? 1 : me[t2];
+      const int d1 = unit ? 1 : ent_exp<PK>(me[t]), d2 = unit ? 1 : ent_exp<PK>(me[t2]);
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
       const E s2 = d2 == 1 ? scale : emul_int(scale, d2);
       deriv_sink(t, emul(s1, g1));
       deriv_sink(t2, emul(s2, g2));
     } else {
-      const int d1 = unit ? 1 : me[t];
+      const int d1 = unit ? 1 : ent_exp<PK>(me[t]);
       const E s1 = d1 == 1 ? scale : emul_int(scale, d1);
       deriv_sink(t, emul(s1, cl[u]));
     }
@@ -695,7 +707,287 @@ __global__ void __launch_bounds__(128) k_segments(long long nseg_total, int m, c
 }
 
 // ---------------------------------------------------------------------------
+// K1+K2 per polynomial in one CTA (k_eval_rows, plan in pn_system::Rows):
+// no contribution buffer in HBM.  A persistent CTA takes whole polynomials;
+// polynomial i is evaluated in chunks of CH = NT/G canonical monomials
+// (aligned power-of-two blocks):
+//   * the chunk's packed support entries (var | slot << 16) arrive in shared
+//     memory by a bulk copy issued one chunk ahead (double buffered, mbarrier);
+//   * mono_tree_eval (identical arithmetic to K1, x staged in shared memory)
+//     stores every derivative at its slot of the chunk buffer, where the
+//     chunk's contributions are ordered by (variable, canonical monomial);
+//   * every variable j then pushes its run of the chunk, in order, onto its
+//     own binary-counter stack in shared memory (level l of variable j at
+//     stk[l * n + j]) -- the streaming form of tree_sum's right-pruned
+//     pairwise order, so the Jacobian entry folded from the stack
+//     at the end is bit-identical to K2's fold of the contiguous run;
+//   * the chunk's monomial values are reduced by the tree's lower levels
+//     (warp shuffles, then the warps' partials) and pushed at chunk
+//     granularity onto a value stack.
+// The row of J is written once (exact zeros included, evaldiff.py:262), f_i
+// and -f_i once.  HBM traffic is the packed supports, the coefficients and
+// the row: the memory-bound complex-double evaluation no longer writes and
+// re-reads (M + nnz) contributions.
 
+// push the run p[0, L) onto a binary-counter stack whose count is c: in
+// aligned blocks of up to 8 (the pairwise node of an aligned block is what
+// the element-wise pushes would build), each block pushed at its level --
+// bit-identical to L element pushes with fewer stack round trips
+template <class E>
+__device__ __forceinline__ void run_push(E *st, int stride, int c, const E *p, int L) {
+  int q = 0;
+  while (q < L) {
+    const int cq = c + q;
+    int l = 0;
+    while (l < 3 && ((cq >> l) & 1) == 0 && q + (2 << l) <= L) ++l;
+    E v;
+    if (l == 0) {
+      v = p[q];
+    } else if (l == 1) {
+      v = eadd(p[q], p[q + 1]);
+    } else if (l == 2) {
+      v = eadd(eadd(p[q], p[q + 1]), eadd(p[q + 2], p[q + 3]));
+    } else {
+      v = eadd(eadd(eadd(p[q], p[q + 1]), eadd(p[q + 2], p[q + 3])),
+               eadd(eadd(p[q + 4], p[q + 5]), eadd(p[q + 6], p[q + 7])));
+    }
+    int lvl = l;
+    for (int k = cq >> l; k & 1; k >>= 1, ++lvl) v = eadd(st[lvl * stride], v);
+    st[lvl * stride] = v;
+    q += 1 << l;
+  }
+}
+
+// in-place right-pruned pairwise tree over p[0, L) (tree_sum order, P4)
+template <class E>
+__device__ __forceinline__ E run_tree_inplace(E *p, int L) {
+  for (int s = 1; s < L; s <<= 1)
+    for (int a = 0; a + s < L; a += 2 * s) p[a] = eadd(p[a], p[a + s]);
+  return p[0];
+}
+
+template <class E, int BASE, int G, int NT, bool XSM>
+__global__ void __launch_bounds__(NT) k_eval_rows(int m, int n, int K, int D, const int64_t *__restrict__ poly_ptr,
+                                                  const int32_t *__restrict__ mon_ptr,
+                                                  const uint32_t *__restrict__ ent, const int32_t *__restrict__ exps,
+                                                  const int32_t *__restrict__ poly_chunk,
+                                                  const int4 *__restrict__ desc,
+                                                  const uint16_t *__restrict__ runoff,
+                                                  const double *__restrict__ coeff, const double *__restrict__ x,
+                                                  const double *__restrict__ table, const int32_t *__restrict__ toff,
+                                                  const double *__restrict__ consts, long long cstride,
+                                                  double *__restrict__ f, double *__restrict__ A, int negf_col,
+                                                  bool unit, BView bv) {
+  constexpr int es = Traits<E>::es;
+  constexpr int CH = NT / G;           // monomials per chunk
+  constexpr int NW = NT / 32;
+  constexpr int VL = RowsLayout::VL;  // value-stack levels (chunk granularity)
+  const int LE = RowsLayout::le(CH, K);  // staged entries per buffer
+  extern __shared__ __align__(16) double rows_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const RowsLayout Lo = rows_layout(n, D, K, es, CH, BASE, NW, XSM);
+  char *sb = reinterpret_cast<char *>(rows_smem);
+  E *xs = reinterpret_cast<E *>(sb + Lo.xs);            // n (when XSM)
+  E *stk = reinterpret_cast<E *>(sb + Lo.stk);          // D x n
+  E *buf = reinterpret_cast<E *>(sb + Lo.buf);          // CH * K chunk contributions (by variable, monomial)
+  E *vals = reinterpret_cast<E *>(sb + Lo.vals);        // CH monomial values
+  E *wpart = reinterpret_cast<E *>(sb + Lo.wpart);      // NW warp partials
+  E *vstk = reinterpret_cast<E *>(sb + Lo.vstk);        // VL
+  int *cnt = reinterpret_cast<int *>(sb + Lo.cnt);      // n
+  uint32_t *sent = reinterpret_cast<uint32_t *>(sb + Lo.sent);  // [2][LE] packed entries
+  int *smp = reinterpret_cast<int *>(sb + Lo.smp);      // [2][lmp] mon_ptr of the chunk
+  double *scf = reinterpret_cast<double *>(sb + Lo.scf);  // [2][lcf] coefficients of the chunk
+  uint16_t *sro = reinterpret_cast<uint16_t *>(sb + Lo.sro);  // [2][rs] run starts of the chunk
+  int *pad = reinterpret_cast<int *>(sb + Lo.pad);      // 2 * BASE: var 0 / exponent 1 for idle groups
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long b = bslot(bv);
+  x += b * bv.x;
+  table += b * bv.t;
+  A += b * bv.a;
+  if (XSM)
+    for (int v = tid; v < n; v += NT) xs[v] = eload<E>(x + (long long)v * es);
+  if (tid < 2 * BASE) pad[tid] = 1 << 28;  // packed: variable 0, slot 0, exponent 1
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const double *xsrc = XSM ? reinterpret_cast<const double *>(xs) : x;
+
+  // Producer (thread 0): stages the CTA's chunks (polynomials blockIdx.x,
+  // +gridDim.x, ...) one chunk ahead -- packed entries, mon_ptr, coefficients
+  // and the variables' run starts, four bulk copies on one mbarrier -- with
+  // the next chunk's descriptor and the next polynomial's chunk range loaded
+  // one step earlier still, so no dependent global load sits on the path.
+  int q_i = blockIdx.x - (int)gridDim.x, q_g = 0, q_ge = 0;
+  int q_ni = blockIdx.x, q_nlo = 0, q_nhi = 0;
+  bool have = false;
+  int4 dnext = make_int4(0, 0, 0, 0);
+  auto prod_next = [&]() -> bool {
+    if (q_g + 1 < q_ge) {
+      ++q_g;
+      return true;
+    }
+    for (;;) {
+      q_i = q_ni;
+      if (q_i >= m) return false;
+      q_g = q_nlo;
+      q_ge = q_nhi;
+      q_ni = q_i + gridDim.x;
+      if (q_ni < m) {
+        q_nlo = poly_chunk[q_ni];
+        q_nhi = poly_chunk[q_ni + 1];
+      }
+      if (q_g < q_ge) return true;
+    }
+  };
+  auto issue = [&](int s) {  // stage chunk q_g (descriptor dnext) into buffer s
+    if (!have) return;
+    const int4 d = dnext;  // {c0, U, e0, e1}
+    const long long c0 = d.x, a0 = d.z & ~3LL, m0 = c0 & ~3LL, f0 = (c0 * es) & ~1LL;
+    // at least 16 bytes (a chunk of constants has no entries; every array carries 16 bytes of padding)
+    const uint32_t be = (uint32_t)max(16LL, ((d.w - a0) * 4 + 15) & ~15LL);
+    const uint32_t bm = (uint32_t)(((c0 + d.y + 1 - m0) * 4 + 15) & ~15LL);
+    const uint32_t bc = (uint32_t)((((c0 + d.y) * es - f0) * 8 + 15) & ~15LL);
+    const uint32_t br = (uint32_t)(Lo.rs * 2);
+    // the buffer's previous contents were read through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bar[s], be + bm + bc + br);
+    bulk_g2s(sent + s * LE, ent + a0, be, &bar[s]);
+    bulk_g2s(smp + s * Lo.lmp, mon_ptr + m0, bm, &bar[s]);
+    bulk_g2s(scf + s * Lo.lcf, coeff + f0, bc, &bar[s]);
+    bulk_g2s(sro + s * Lo.rs, runoff + (long long)q_g * Lo.rs, br, &bar[s]);
+    have = prod_next();
+    if (have) dnext = desc[q_g];
+  };
+  if (tid == 0) {
+    if (q_ni < m) {
+      q_nlo = poly_chunk[q_ni];
+      q_nhi = poly_chunk[q_ni + 1];
+    }
+    have = prod_next();
+    if (have) dnext = desc[q_g];
+    issue(0);
+  }
+  uint32_t phase[2] = {0, 0};
+  int s = 0;
+
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    const long long p0 = poly_ptr[i];
+    const int T = (int)(poly_ptr[i + 1] - p0);
+    const int nch = (T + CH - 1) / CH;
+    for (int j = tid; j < n; j += NT) cnt[j] = 0;
+    E value = ezero<E>();  // f_i; zero_like for an empty polynomial (evaldiff.py:261)
+    for (int c = 0; c < nch; ++c, s ^= 1) {
+      // stage the chunk after this one into the other buffer (released by the
+      // barrier that ended the previous chunk)
+      if (tid == 0) issue(s ^ 1);
+      const long long c0 = p0 + (long long)c * CH;
+      const int U = min(CH, T - c * CH);
+      mbar_wait(&bar[s], phase[s]);
+      phase[s] ^= 1;
+      const int *mp = smp + s * Lo.lmp + (int)(c0 & 3);        // mon_ptr[c0 + u] = mp[u]
+      const double *cf = scf + s * Lo.lcf + (int)((c0 * es) & 1);  // coefficient u at cf + u * es
+      const int e0 = mp[0], shift = e0 & 3;
+      // ---- trees: group u of G lanes takes monomial u of the chunk
+      const int u = tid / G, r = tid % G;
+      const int uu = u < U ? u : 0;
+      const int lo = mp[uu] - e0 + shift, k = mp[uu + 1] - mp[uu];
+      const bool tree = u < U && k > 0;
+      if (u < U && k == 0 && r == 0)  // constant term (evaldiff.py:152-153); per-start shift if given
+        vals[u] = consts ? eload<E>(consts + b * cstride + (long long)i * es) : eload<E>(cf + uu * es);
+      const int32_t *mv = tree ? reinterpret_cast<const int32_t *>(sent + s * LE + lo) : pad;
+      const E co = tree ? eload<E>(cf + uu * es) : ezero<E>();
+      mono_tree_eval<E, BASE, G, 1, XSM>(
+          r, tree, tree ? k : BASE, mv, mv, co, xsrc, table, toff, [&](const E &v) { vals[u] = v; },
+          [&](int t, const E &v) { buf[ent_slot<1>(mv[t])] = v; }, unit);
+      __syncthreads();
+      // ---- pushes: variable j's run of this chunk, in canonical order
+      const uint16_t *ro = sro + s * Lo.rs;
+      for (int j = tid; j < n; j += NT) {
+        const int a = ro[j], L = ro[j + 1] - a;
+        if (L == 0) continue;
+        run_push(stk + j, n, cnt[j], buf + a, L);
+        cnt[j] += L;
+      }
+      // ---- values: the chunk's node of tree_sum (aligned block of CH)
+      {
+        E v = tid < U ? vals[tid] : ezero<E>();
+        if (warp * 32 < U) {
+#pragma unroll
+          for (int w = 1; w < 32; w <<= 1) {
+            const E o = eshfl_down(v, w);
+            if ((lane & (2 * w - 1)) == 0 && lane + w < U - warp * 32) v = eadd(v, o);
+          }
+          if (lane == 0) wpart[warp] = v;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        const int P = (U + 31) / 32;
+        E v = run_tree_inplace(wpart, P);
+        if (c + 1 < nch) {
+          stack_push(vstk, 1, c, v);
+        } else {  // last chunk: fold the chunk-level counter (c full chunks)
+          E acc = v;
+          for (int l = 0; l < VL; ++l)
+            if ((c >> l) & 1) acc = eadd(vstk[l], acc);
+          value = acc;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- the row: J[i, :] column-major (ld = m), f_i, -f_i
+    for (int j = tid; j < n; j += NT) {
+      const int L = cnt[j];
+      estore(A + ((long long)j * m + i) * es, L ? stack_fold(stk + j, n, L) : ezero<E>());
+    }
+    if (tid == 0) {
+      if (f) estore(f + b * bv.f + (long long)i * es, value);
+      if (negf_col >= 0) estore(A + ((long long)negf_col * m + i) * es, eneg(value));
+    }
+    __syncthreads();  // cnt / stacks are reset by the next polynomial
+  }
+}
+
+template <class E, int BASE>
+static size_t rows_smem(const pn_system *sys, int NT, int G, bool xsm) {
+  return rows_layout(sys->n, sys->rows.D, sys->rows.K, Traits<E>::es, NT / G, BASE, NT / 32, xsm).total;
+}
+
+template <class E, int BASE>
+static void launch_rows(pn_system *sys, const double *x, const double *table, double *f, double *A, int negf_col,
+                        int nb, const BView &bv, const double *consts, long long cstride, cudaStream_t st) {
+  constexpr int G = rows_g(Traits<E>::nc, Traits<E>::cplx, BASE);
+  constexpr int NT = rows_nt(Traits<E>::nc);
+  const auto &R = sys->rows;
+  // x in shared memory when it fits beside the stacks
+  const bool xsm = rows_smem<E, BASE>(sys, NT, G, true) <= kRowsSmemMax;
+  const size_t smem = rows_smem<E, BASE>(sys, NT, G, xsm);
+  auto kern = xsm ? k_eval_rows<E, BASE, G, NT, true> : k_eval_rows<E, BASE, G, NT, false>;
+  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  const int want = std::max(1, per_sm * num_sms() / std::max(nb, 1));
+  const dim3 grid((unsigned)std::min(sys->m, want), (unsigned)nb);
+  kern<<<grid, NT, smem, st>>>(sys->m, sys->n, R.K, R.D, sys->d_seg_ptr, sys->d_mon_ptr, R.d_ent, sys->d_exp,
+                               R.d_poly_chunk, R.d_desc, R.d_runoff, sys->d_coeff, x, table, sys->d_toff, consts, cstride, f,
+                               A, negf_col, R.unit, bv);
+  PN_CHECK_LAUNCH();
+  count_launch(1);
+}
+
+// the row path serves systems it was planned for (uniform k, stacks fit);
+// PN_EVAL_ROWS=0|1 at call time overrides the default (complex/real
+// double: memory-bound; dd/qd keep the FP64-bound K1 + K2 unless forced)
+template <class E>
+static bool use_rows(const pn_system *sys) {
+  if (!sys->rows.ok) return false;
+  const char *v = getenv("PN_EVAL_ROWS");
+  if (v) return strcmp(v, "0") != 0;
+  return Traits<E>::nc == 1;
+}
 
 template <class E, int BASE>
 static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double *x, const double *table,
@@ -792,6 +1084,16 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
     k_power_table<E><<<dim3((sys->n + 127) / 128, nb), 128, 0, st>>>(sys->n, x, sys->d_toff, sys->d_tdeg, table, bv);
     PN_CHECK_LAUNCH();
     count_launch(1);
+  }
+  if (use_rows<E>(sys)) {
+    switch (sys->rows.base) {
+      case 2: launch_rows<E, 2>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 4: launch_rows<E, 4>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 8: launch_rows<E, 8>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      case 16: launch_rows<E, 16>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+      default: launch_rows<E, 32>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
+    }
+    return;
   }
   if (use_fused<E>(sys, nb, bv)) {
     switch (sys->fused.base) {

@@ -133,6 +133,52 @@ void backsub_device(int nc, int cplx, int n, const double *R, double *x, MgsWork
 // read the status record written by mgs/backsub; returns PN_OK / PN_E_BREAKDOWN / PN_E_SINGULAR
 int mgs_read_status(MgsWork &w, pn_numinfo *info, cudaStream_t st);
 
+// k_eval_rows geometry: CTA size and lanes per monomial (chunk = NT / G
+// monomials).  Plain double: 8 lanes per monomial so 1024 threads fit the
+// register file (twice the warps to hide the stack pushes' latency).
+__host__ __device__ constexpr int rows_nt(int nc) { return nc == 1 ? 1024 : 512; }
+__host__ __device__ constexpr int rows_g(int nc, bool cplx, int base) {
+  return (nc == 1 || nc == 4 || (nc == 2 && cplx) ? 8 : 4) < base ? (nc == 1 || nc == 4 || (nc == 2 && cplx) ? 8 : 4)
+                                                                     : base;
+}
+
+// shared-memory carve-up of k_eval_rows (byte offsets, 16-byte aligned),
+// shared by the plan (system.cu) and the kernel (evaldiff.cu)
+constexpr size_t kRowsSmemMax = 226 * 1024;
+struct RowsLayout {
+  static constexpr int VL = 24;  // value-stack levels
+  static constexpr __host__ __device__ int le(int CH, int K) { return CH * K + 8; }  // staged entries per buffer
+  size_t xs, stk, buf, vals, wpart, vstk, cnt, sent, smp, scf, sro, pad, total;
+  int lmp, lcf, rs;  // per-buffer lengths: mon_ptr ints, coefficient doubles, run starts (uint16)
+};
+__host__ __device__ inline RowsLayout rows_layout(int n, int D, int K, int es, int CH, int BASE, int NW, bool xsm) {
+  RowsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = (o + bytes + 15) & ~(size_t)15;
+    return at;
+  };
+  const size_t eb = (size_t)es * 8;
+  L.xs = take(xsm ? (size_t)n * eb : 0);
+  L.stk = take((size_t)D * n * eb);
+  L.buf = take((size_t)CH * K * eb);
+  L.vals = take((size_t)CH * eb);
+  L.wpart = take((size_t)NW * eb);
+  L.vstk = take((size_t)RowsLayout::VL * eb);
+  L.cnt = take((size_t)n * 4);
+  L.sent = take((size_t)2 * RowsLayout::le(CH, K) * 4);
+  L.lmp = CH + 8;
+  L.lcf = ((CH + 1) * es + 3) & ~1;
+  L.rs = (n + 1 + 7) & ~7;
+  L.smp = take((size_t)2 * L.lmp * 4);
+  L.scf = take((size_t)2 * L.lcf * 8);
+  L.sro = take((size_t)2 * L.rs * 2);
+  L.pad = take((size_t)2 * BASE * 4);
+  L.total = o;
+  return L;
+}
+
 }  // namespace pn
 
 // ---------------------------------------------------------------------------
@@ -185,6 +231,22 @@ struct pn_system {
     int16_t *d_ldst = nullptr;
     int32_t *d_seg_var = nullptr, *d_seg_sl = nullptr, *d_chunk_seg = nullptr, *d_poly_chunk = nullptr;
   } fused;
+
+  // plan of the row evaluation (k_eval_rows): one CTA per polynomial at a
+  // time, chunks of CH canonical monomials, per-variable binary-counter
+  // stacks of depth D in shared memory.  Applies when every non-constant
+  // monomial has the same k = K (2..32), n <= 65536, exponents <= 15 and the
+  // stacks fit.
+  struct Rows {
+    bool ok = false;
+    int K = 0, base = 0, CH = 0, D = 0;
+    long long nchunks = 0;
+    bool unit = false;             // every exponent is 1
+    uint32_t *d_ent = nullptr;     // nnz: var | (slot in the chunk buffer) << 16 | exponent << 28
+    int32_t *d_poly_chunk = nullptr;  // m + 1: first chunk of each polynomial
+    int4 *d_desc = nullptr;        // nchunks: {first monomial, monomials, first entry, end entry}
+    uint16_t *d_runoff = nullptr;  // nchunks * rs (rs = n + 1 rounded up to 8): start of variable j's run
+  } rows;
 
   // scratch reused across evaluations
   pn::DevArena contrib;  // (M + nnz) * es

@@ -36,6 +36,10 @@ pn_system::~pn_system() {
   cudaFree(fused.d_seg_sl);
   cudaFree(fused.d_chunk_seg);
   cudaFree(fused.d_poly_chunk);
+  cudaFree(rows.d_ent);
+  cudaFree(rows.d_poly_chunk);
+  cudaFree(rows.d_desc);
+  cudaFree(rows.d_runoff);
   if (ev) cudaEventDestroy(ev);
   if (step_graph) cudaGraphExecDestroy(step_graph);
   for (auto e : gev)
@@ -156,6 +160,91 @@ void build_fused_plan(pn_system &S, const int32_t *poly_ptr, const std::vector<i
   F.d_chunk_seg = upload(chunk_seg);
   F.d_poly_chunk = upload(poly_chunk);
   F.ok = true;
+}
+
+
+// Plan of the row evaluation (evaldiff.cu, k_eval_rows).  Eligible when
+// every non-constant monomial has the same k = K (2 <= K <= 32), n fits 16
+// bits and the per-variable stacks (n x D elements, D = bit length of the
+// longest Jacobian-entry run) fit in shared memory.  Chunks are CH = 512/G
+// consecutive canonical monomials of a polynomial (rows_nt / rows_g in
+// internal.h); inside a chunk the support entries are ranked by
+// (variable, monomial) -- the reference's summation order restricted to the
+// chunk (evaldiff.py:252-265) -- and each entry is packed as
+// var | rank << 16 | exponent << 28 (rank < CH * K <= 4096); per chunk the
+// run start of every variable (uint16).
+void build_rows_plan(pn_system &S, const int32_t *poly_ptr, const std::vector<int32_t> &cptr,
+                     const std::vector<int32_t> &cvar, const std::vector<int32_t> &cexp) {
+  const char *env = getenv("PN_EVAL_ROWS");
+  if (env && strcmp(env, "0") == 0) return;
+  const int m = S.m, n = S.n, es = S.es;
+  if (m == 0 || n > 65536) return;
+  int K = -1;
+  for (int64_t c = 0; c < S.M; ++c) {
+    const int k = cptr[c + 1] - cptr[c];
+    if (k == 0) continue;
+    if (K < 0) K = k;
+    else if (k != K) return;
+  }
+  if (K < 2 || K > 32) return;
+  const int base = floor_pow2(K);
+  const int G = rows_g(S.nc, S.cplx, base), NT = rows_nt(S.nc);
+  const int CH = NT / G;
+  // stack depth
+  std::vector<int32_t> cnt(n, 0);
+  int maxL = 0;
+  for (int i = 0; i < m; ++i) {
+    for (int32_t t = cptr[poly_ptr[i]]; t < cptr[poly_ptr[i + 1]]; ++t) maxL = std::max(maxL, ++cnt[cvar[t]]);
+    for (int32_t t = cptr[poly_ptr[i]]; t < cptr[poly_ptr[i + 1]]; ++t) cnt[cvar[t]] = 0;
+  }
+  int D = 1;
+  while ((1 << D) <= maxL) ++D;
+  for (int64_t t = 0; t < S.nnz; ++t)
+    if (cexp[t] > 15) return;  // 4 exponent bits in the packed entry
+  // shared memory without x staged (evaldiff.cu decides whether x fits too)
+  if (rows_layout(n, D, K, es, CH, base, NT / 32, false).total > kRowsSmemMax) return;
+  std::vector<int32_t> poly_chunk(m + 1, 0);
+  for (int i = 0; i < m; ++i) poly_chunk[i + 1] = poly_chunk[i] + (poly_ptr[i + 1] - poly_ptr[i] + CH - 1) / CH;
+  const long long nchunks = poly_chunk[m];
+  const int RS = (n + 1 + 7) & ~7;
+  std::vector<uint32_t> ent(S.nnz);
+  std::vector<uint16_t> runoff((size_t)nchunks * RS);
+  std::vector<int4> desc(nchunks);
+  std::vector<int32_t> pos(n);
+  for (int i = 0; i < m; ++i) {
+    const int T = poly_ptr[i + 1] - poly_ptr[i];
+    for (int c = 0; c * CH < T; ++c) {
+      const int64_t c0 = poly_ptr[i] + (int64_t)c * CH, c1 = std::min<int64_t>(poly_ptr[i + 1], c0 + CH);
+      const int32_t e0 = cptr[c0], e1 = cptr[c1];
+      for (int32_t t = e0; t < e1; ++t) cnt[cvar[t]]++;
+      desc[poly_chunk[i] + c] = make_int4((int)c0, (int)(c1 - c0), e0, e1);
+      uint16_t *ro = &runoff[(size_t)(poly_chunk[i] + c) * RS];
+      int acc = 0;
+      for (int j = 0; j < n; ++j) {
+        ro[j] = (uint16_t)acc;
+        pos[j] = acc;
+        acc += cnt[j];
+        cnt[j] = 0;
+      }
+      ro[n] = (uint16_t)acc;
+      for (int32_t t = e0; t < e1; ++t)
+        ent[t] = (uint32_t)cvar[t] | ((uint32_t)pos[cvar[t]]++ << 16) | ((uint32_t)cexp[t] << 28);
+    }
+  }
+  bool unit = true;
+  for (int64_t t = 0; unit && t < S.nnz; ++t) unit = cexp[t] == 1;
+  auto &R = S.rows;
+  R.K = K;
+  R.base = base;
+  R.CH = CH;
+  R.D = D;
+  R.nchunks = nchunks;
+  R.unit = unit;
+  R.d_ent = upload(ent);
+  R.d_poly_chunk = upload(poly_chunk);
+  R.d_runoff = upload(runoff);
+  R.d_desc = upload(desc);
+  R.ok = true;
 }
 
 }  // namespace
@@ -358,6 +447,7 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
   S.d_seg_ptr = upload(seg_ptr);
   S.d_seg_out = upload(seg_out);
   build_fused_plan(S, poly_ptr, cptr, cvar);
+  build_rows_plan(S, poly_ptr, cptr, cvar, cexp);
   PN_CHECK_CUDA(cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
   *out = sys.release();
   PN_API_END
@@ -376,6 +466,14 @@ extern "C" int pn_system_get_stats(const pn_system *sys, pn_system_stats *stats)
   PN_API_BEGIN
   PN_REQUIRE(sys && stats, PN_E_ARG, "NULL argument");
   *stats = sys->stats;
+  PN_API_END
+}
+
+extern "C" int pn_system_plan_info(const pn_system *sys, pn_plan_info *info) {
+  PN_API_BEGIN
+  PN_REQUIRE(sys && info, PN_E_ARG, "NULL argument");
+  const auto &R = sys->rows;
+  *info = pn_plan_info{R.ok ? 1 : 0, R.K, R.CH, R.D, (int64_t)R.nchunks};
   PN_API_END
 }
 

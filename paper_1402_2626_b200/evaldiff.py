@@ -86,6 +86,12 @@ class PreparedSystem:
         _lib.check(_lib.load().pn_system_get_stats(self._handle, ctypes.byref(s)))
         return s
 
+    def rows_plan(self) -> dict:
+        """The row-evaluation plan of this system (pn_system_plan_info)."""
+        pi = _lib.PlanInfo()
+        _lib.check(_lib.load().pn_system_plan_info(self._handle, ctypes.byref(pi)))
+        return {"ok": bool(pi.rows_ok), "K": pi.K, "chunk": pi.chunk, "depth": pi.depth, "nchunks": pi.nchunks}
+
     def close(self):
         if getattr(self, "_handle", None) and self._handle.value:
             _lib.load().pn_system_destroy(self._handle)

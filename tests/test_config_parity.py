@@ -173,7 +173,8 @@ def _packed_rows(level, n, supports, coeffs):
 @pytest.mark.parametrize("lv", ["rdd", "cqd", "cdd"])
 @pytest.mark.parametrize("k", [512, 1024, 2048, 4096])
 def test_single_large_monomial_vs_oracle(gpu, lv, k):
-    """One monomial of k variables at x_j = 1 + j/k (test_acceptance.py:46-61):
+    """One monomial of k variables at x_j = 1 + j/(64k) (the shape of
+    test_acceptance.py:46-61, scaled so the k = 4096 product stays finite):
     value, all k partial derivatives and the analytic counts: the product
     tree's k-1 / 2k-4 (test_acceptance.py:46-61) plus the k coefficient
     scalings of eval_monomial_and_derivs, i.e. k / 3k-4 (k a power of two).
@@ -185,7 +186,7 @@ def test_single_large_monomial_vs_oracle(gpu, lv, k):
     coeffs.reshape(level.es, 1)[0, 0] = 1.0
     p = _packed_rows(level, k, [[list(range(k))]], coeffs)
     x = np.zeros(level.cshape + (k,))
-    x.reshape(level.es, k)[0] = 1.0 + np.arange(k) / k
+    x.reshape(level.es, k)[0] = 1.0 + np.arange(k) / (64.0 * k)
     if level.cplx:
         x[1, 0] = 1e-3 * np.cos(np.arange(k))
     ev = evaluate_system(PreparedSystem(p), x)
