@@ -217,8 +217,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// The CTA barrier orders every thread's Q/R stores before thread 0's
+// release store (gpu scope, cumulative), so one fence in thread 0 suffices
+// instead of a MEMBAR.GPU in every thread (the CUTLASS semaphore pattern).
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void publish(int *ready, int k) {
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     st_release(ready + k, 1);
@@ -905,9 +910,8 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
 #pragma unroll
       for (int q = 0; q < B; ++q)
         if (q < valid) estore(qc + (long long)(row0 + q) * es, ediv_prepared(a[q], p));
-      __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(ready + j, 1);
+      if (tid == 0) red_release_add(ready + j, 1);
     }
   }
   cl_sync();  // keep the exchange slots alive until every peer has read them
@@ -1057,8 +1061,11 @@ __global__ void __launch_bounds__(32) k_mgs_warp(double *__restrict__ A, int m, 
 // CTA knows the order of its (sweep, column) applies in advance, so the next
 // column is brought into a second shared-memory buffer by a cp.async.bulk
 // (TMA) while the current one computes, and q_k arrives the same way once per
-// sweep.  Thread t owns rows t, t+256, ... (one row of each 256-row block),
-// which keeps shared-memory reads conflict-free on the bulk-copied layout;
+// sweep.  Thread t owns rows t, t+256, ... (one row of each 256-row block).
+// For double double the element accesses conflict (ncu r01: 570 M excess
+// wavefronts); a lane-rotated 16-byte access order removed 88 % of them but
+// made the kernel 6 % slower (the selects cost more than the conflicts: it is
+// barrier and FP64 bound, ncu r02), so the plain layout stays;
 // each block's dot product is a block tree, reduced for all blocks at once by
 // the warp reduce-scatter, and the block sums are combined pairwise (aligned
 // 256-row blocks: the top levels of tree_sum's tree).  Column updates are
