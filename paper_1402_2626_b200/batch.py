@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .evaldiff import PreparedSystem
+from .evaldiff import PreparedSystem, point_planes
 from .polyrep import PackedSystem
 from .varith import VecContext
 from .xprec import PrecisionLevel
@@ -45,8 +45,11 @@ def shard_range(B: int, world: int, rank: int) -> tuple:
 def evaluate_batch(prep: PreparedSystem, X: np.ndarray) -> np.ndarray:
     """f(x_b) for X planes cshape + (B, n) -> planes cshape + (B, m)."""
     level = prep.level
-    B = X.shape[-2]
     X = np.ascontiguousarray(X, dtype=np.float64)
+    if X.ndim < 2:
+        raise ValueError("X must be planes cshape + (B, n)")
+    B = X.shape[-2]
+    X = point_planes(X, level, prep.n_vars, B)
     F = np.empty(level.cshape + (B, prep.n_eqs))
     _lib.check(_lib.load().pn_evaldiff_batch(prep.handle, B, _lib.ptr(X), _lib.ptr(F), None))
     return F
@@ -127,7 +130,12 @@ def run_newton_batch(prep: PreparedSystem, X0: np.ndarray, consts: np.ndarray | 
     """B independent Newton runs on the GPU (pn_newton_batch)."""
     level = prep.level
     X0 = np.ascontiguousarray(X0, dtype=np.float64)
+    if X0.ndim < 2:
+        raise ValueError("X0 must be planes cshape + (B, n)")
     B = X0.shape[-2]
+    X0 = point_planes(X0, level, prep.n_vars, B)
+    if consts is not None:
+        consts = point_planes(consts, level, prep.n_eqs, B)
     X = np.empty_like(X0)
     iters = np.zeros(B, np.int32)
     status = np.zeros(B, np.int32)
@@ -178,3 +186,34 @@ def gather_batch(shard: BatchResult, B: int, group=None) -> BatchResult:
         out[key] = np.concatenate(parts, axis=0 if key == "x" else -1)
     x = np.moveaxis(out["x"], 0, 1).reshape(cshape + (B, n))
     return BatchResult(np.ascontiguousarray(x), out["iters"].astype(np.int32), out["status"].astype(np.int32))
+
+
+def _prepare_shard(packed: PackedSystem, Zs: np.ndarray, t):
+    system, consts = homotopy_batch(packed, Zs, t)
+    return PreparedSystem(system), consts
+
+
+def run_batched(packed: PackedSystem, Z: np.ndarray, t, max_iters: int = 10, tol: float | None = None,
+                group=None, prepare=None, solve=None):
+    """Config C5 on this rank: the B starts Z (planes cshape + (B, n)) are
+    split by shard_range over the process group, the rank builds the
+    homotopy constants of its shard (homotopy_start_system semantics,
+    newton.py:135-159), runs its batch of run_newton (newton.py:106-132)
+    and all ranks all_gather status, iterations and final x once (the only
+    collective).  Returns (shard_result, full_result, (lo, hi)).
+
+    ``prepare(packed, Zs, t) -> (prep, consts)`` and ``solve(prep, Zs,
+    consts, max_iters=, tol=) -> BatchResult`` default to the GPU path; the
+    CPU tests substitute stubs to check the orchestration with gloo."""
+    import torch.distributed as dist
+    init = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if init else 1
+    rank = dist.get_rank(group) if init else 0
+    B = Z.shape[-2]
+    lo, hi = shard_range(B, world, rank)
+    Zs = np.ascontiguousarray(Z[..., lo:hi, :])
+    prep, consts = (prepare or _prepare_shard)(packed, Zs, t)
+    shard = (solve or run_newton_batch)(prep, Zs, consts, max_iters=max_iters, tol=tol)
+    full = gather_batch(shard, B, group) if init else shard
+    return shard, full, (lo, hi)
+

@@ -330,14 +330,11 @@ void solve_batch_impl(int nb, const int32_t *slots, int m, int n, double *A, lon
   PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
   PN_REQUIRE(m <= 1024, PN_E_ARG, "batched solve supports m <= 1024 rows (got %d)", m);
   if (nb <= 0) return;
-  // default "narrow": half the panel width and two CTAs per SM (more warps
-  // to hide FP64 latency, twice the Q traffic): 3524 vs 3120 start-iterations/s
-  // on C5 (profiles/r01); "wide" = full panel, one CTA per SM
-  const char *v = getenv("PN_SOLVE_VARIANT");
-  const bool narrow = !(v && strcmp(v, "wide") == 0);
+  // half the panel width and two CTAs per SM at m <= 256 (more warps to hide
+  // FP64 latency, twice the Q traffic): 3524 vs 3120 start-iterations/s on
+  // C5 against the full panel (r01)
   if (m <= 256) {
-    if (narrow) launch_solve<E, 1, PM / 2, 2>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
-    else launch_solve<E, 1, PM, 1>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
+    launch_solve<E, 1, PM / 2, 2>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
   } else if (m <= 512) {
     launch_solve<E, 2, PM / 2, 1>(nb, slots, m, n, A, As, Q, Qs, R, Rs, x, xs, dx, eps, tol, flags, st);
   } else {

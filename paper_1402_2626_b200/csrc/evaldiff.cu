@@ -279,18 +279,7 @@ __global__ void __launch_bounds__(NT) k_mono_tree(const int32_t *__restrict__ li
 }
 
 // ---------------------------------------------------------------------------
-// Fused evaluation for batches (config C5): one CTA per (polynomial, slot)
-// evaluates the polynomial's monomials chunk by chunk (CH = NT/G monomials
-// in canonical order, supports staged in shared memory) and folds every
-// contribution straight into per-variable binary-counter stacks in shared
-// memory -- the streaming form of tree_sum's pairwise order --
-// so f and the Jacobian row never round-trip through a contribution buffer.
-// Within a chunk the derivative contributions land in (var, monomial) order
-// (host-computed ldst), each variable's run is pushed by one thread, and the
-// chunk's values are reduced by a warp tree and pushed at chunk granularity
-// (full chunks are aligned blocks of the counter).  Systems whose monomials
-// all have k in {0, K} (2 <= K <= 32) and whose stacks fit shared memory use
-// this path (pn_system::Fused); everything else uses K1 + K2.
+// lanes per monomial of the K1 trees, by precision
 
 template <class E> struct TreeG;  // lanes per monomial, by precision
 #ifndef PN_TREE_G_DD
@@ -319,144 +308,6 @@ __device__ __forceinline__ E stack_fold(const E *st, int stride, int cnt) {
   return acc;
 }
 
-template <class E, int BASE, int G, int NT>
-__global__ void __launch_bounds__(NT) k_eval_fused(int m, int n, int D, int K, const int64_t *__restrict__ poly_ptr,
-                                                   const int32_t *__restrict__ mon_ptr,
-                                                   const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
-                                                   const int16_t *__restrict__ ldst, const double *__restrict__ coeff,
-                                                   const int32_t *__restrict__ seg_var,
-                                                   const int32_t *__restrict__ seg_sl,
-                                                   const int32_t *__restrict__ chunk_seg,
-                                                   const int32_t *__restrict__ poly_chunk,
-                                                   const double *__restrict__ x, const double *__restrict__ table,
-                                                   const int32_t *__restrict__ toff, const double *__restrict__ consts,
-                                                   long long cstride, double *__restrict__ f, double *__restrict__ A,
-                                                   int negf_col, BView bv) {
-  constexpr int es = Traits<E>::es;
-  constexpr int CH = NT / G;
-  constexpr int VL = 24;  // value-stack levels (chunk granularity)
-  extern __shared__ __align__(16) double fz_smem[];
-  E *stk = reinterpret_cast<E *>(fz_smem);            // D levels x n variables (level-major)
-  E *buf = stk + (size_t)n * D;                       // CH values + CH*K derivatives
-  E *vstk = buf + CH * (1 + K);                       // VL
-  int *cnt = reinterpret_cast<int *>(vstk + VL);      // n
-  // supports of the chunk, monomial u at u*KP (KP = K+1: odd stride, no bank conflicts)
-  const int KP = K + 1;
-  int *svar = cnt + n;                                // CH*KP + 32 (zero pad)
-  int *sexp = svar + CH * KP + 32;
-  int *sdst = sexp + CH * KP + 32;
-  const int PAD = CH * KP;
-
-  const int i = blockIdx.x;
-  const long long b = bslot(bv);
-  x += b * bv.x;
-  table += b * bv.t;
-  A += b * bv.a;
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int j = tid; j < n; j += NT) cnt[j] = 0;
-  if (tid < 32) {
-    svar[PAD + tid] = 0;  // inactive groups read this pad
-    sexp[PAD + tid] = 1;
-  }
-  const long long p0 = poly_ptr[i];
-  const int T = (int)(poly_ptr[i + 1] - p0);
-  const int gc0 = poly_chunk[i], nch = poly_chunk[i + 1] - gc0;
-  E value = ezero<E>();  // f_i; zero_like for an empty polynomial (evaldiff.py:261)
-  for (int c = 0; c < nch; ++c) {
-    const long long cm0 = p0 + (long long)c * CH;
-    const int U = min(CH, T - c * CH);
-    const int e0 = mon_ptr[cm0], ne = mon_ptr[cm0 + U] - e0;
-    __syncthreads();  // the previous chunk's pushes are done with buf / supports
-    int lead = 0;  // constant monomials sort first (k = 0, no support entries)
-    while (lead < U && mon_ptr[cm0 + lead + 1] == e0) ++lead;
-    for (int e = tid; e < ne; e += NT) {
-      const int pos = (lead + e / K) * KP + e % K;
-      svar[pos] = var[e0 + e];
-      sexp[pos] = exps[e0 + e];
-      sdst[pos] = CH + ldst[e0 + e];
-    }
-    __syncthreads();
-    // ---- monomials: group g of G lanes takes monomial u = g of the chunk
-    const int u = tid / G, r = tid % G;
-    const long long cm = cm0 + (u < U ? u : 0);
-    const int lo = mon_ptr[cm], k = mon_ptr[cm + 1] - lo;
-    const bool tree = u < U && k > 0;
-    if (u < U && k == 0 && r == 0) {  // constant term (evaldiff.py:152-153); per-start shift if given
-      buf[u] = consts ? eload<E>(consts + b * cstride + (long long)i * es) : eload<E>(coeff + cm * es);
-    }
-    const int off = tree ? u * KP : PAD;
-    const E co = tree ? eload<E>(coeff + cm * es) : ezero<E>();
-    mono_tree_eval<E, BASE, G>(
-        r, tree, tree ? k : BASE, svar + off, sexp + off, co, x, table, toff, [&](const E &v) { buf[u] = v; },
-        [&](int t, const E &v) { buf[sdst[off + t]] = v; });
-    __syncthreads();
-    // ---- per-variable pushes, one thread per variable run of the chunk
-    const int s0 = chunk_seg[gc0 + c], s1 = chunk_seg[gc0 + c + 1];
-    for (int s = s0 + tid; s < s1; s += NT) {
-      const int j = seg_var[s], sl = seg_sl[s];
-      const int st = sl & 0xffff, len = sl >> 16;
-      int cj = cnt[j];
-      for (int q = 0; q < len; ++q, ++cj) stack_push(stk + j, n, cj, buf[CH + st + q]);
-      cnt[j] = cj;
-    }
-    // ---- values: warp tree of the chunk (right-pruned), pushed per chunk
-    if (tid < 32) {
-      E v = lane < U ? buf[lane] : ezero<E>();
-#pragma unroll
-      for (int s = 1; s < 32; s <<= 1) {
-        const E o = eshfl_down(v, s);
-        if ((lane & (2 * s - 1)) == 0 && lane + s < U) v = eadd(v, o);
-      }
-      if (lane == 0) {
-        if (c + 1 < nch) {
-          stack_push(vstk, 1, c, v);
-        } else {  // last chunk: fold the chunk-level counter (c full chunks)
-          E acc = v;
-          for (int l = 0; l < VL; ++l)
-            if ((c >> l) & 1) acc = eadd(vstk[l], acc);
-          value = acc;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // ---- Jacobian row i (column-major, ld = m) and the b column
-  for (int j = tid; j < n; j += NT) {
-    const int L = cnt[j];
-    estore(A + ((long long)j * m + i) * es, L ? stack_fold(stk + j, n, L) : ezero<E>());
-  }
-  if (tid == 0) {
-    if (f) estore(f + b * bv.f + (long long)i * es, value);
-    if (negf_col >= 0) estore(A + ((long long)negf_col * m + i) * es, eneg(value));
-  }
-}
-
-template <class E>
-static size_t fused_smem(const pn_system *sys) {
-  constexpr int es = Traits<E>::es;
-  const int CH = 32, K = sys->fused.K;
-  return (size_t)es * 8 * ((size_t)sys->n * sys->fused.D + CH * (1 + K) + 24) +
-         4 * ((size_t)sys->n + 3 * (CH * (K + 1) + 32));
-}
-
-template <class E, int BASE>
-static void launch_fused(pn_system *sys, const double *x, const double *table, double *f, double *A, int negf_col,
-                         int nb, const BView &bv, const double *consts, long long cstride, cudaStream_t st) {
-  constexpr int G = TreeG<E>::value < BASE ? TreeG<E>::value : BASE;
-  constexpr int NT = 32 * G;
-  static_assert(NT / G == 32, "fused chunks are 32 monomials");
-  const size_t smem = fused_smem<E>(sys);
-  auto kern = k_eval_fused<E, BASE, G, NT>;
-  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const auto &F = sys->fused;
-  kern<<<dim3(sys->m, nb), NT, smem, st>>>(sys->m, sys->n, F.D, F.K, sys->d_seg_ptr, sys->d_mon_ptr, sys->d_var,
-                                          sys->d_exp, F.d_ldst, sys->d_coeff, F.d_seg_var, F.d_seg_sl,
-                                          F.d_chunk_seg, F.d_poly_chunk, x, table, sys->d_toff, consts, cstride, f,
-                                          A, negf_col, bv);
-  PN_CHECK_LAUNCH();
-  count_launch(1);
-}
-
 // ---------------------------------------------------------------------------
 // K1 with TMA-staged supports (dense uniform buckets: every monomial of the
 // bucket has k = K and the bucket's support entries are one contiguous block,
@@ -473,15 +324,12 @@ __global__ void __launch_bounds__(NT, MINB) k_mono_tree_tma(const int32_t *__res
                                                       const int32_t *__restrict__ dst, const double *__restrict__ coeff,
                                                       const double *__restrict__ x, const double *__restrict__ table,
                                                       const int32_t *__restrict__ toff, double *__restrict__ contrib,
-                                                      BView bv, int KS, bool unit) {
+                                                      BView bv, bool unit) {
   constexpr int es = Traits<E>::es;
   constexpr int CH = NT / G;
   extern __shared__ __align__(16) int tma_smem[];
   __shared__ __align__(8) uint64_t bar[2];
-  // KS: shared-memory row stride of a monomial's support.  KS == K: the chunk
-  // arrives as one contiguous copy per array; otherwise (KS = G mod 32) row by
-  // row, so the 32/G monomials of a warp read distinct banks.
-  const int L = CH * KS;                       // ints per array per stage (multiple of 4)
+  const int L = CH * K;                        // ints per array per stage (multiple of 4)
   int *st_var = tma_smem;                      // [2][L]
   int *st_exp = st_var + 2 * L;                // [2][L]
   int *st_dst = st_exp + 2 * L;                // [2][L]
@@ -500,50 +348,33 @@ __global__ void __launch_bounds__(NT, MINB) k_mono_tree_tma(const int32_t *__res
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](long long ch, int s) {  // warp 0: stage chunk ch into buffer s
+  auto issue = [&](long long ch, int s) {  // thread 0: stage chunk ch into buffer s
     const long long m0 = ch * CH;
     const int cnt = (int)min((long long)CH, count - m0);
     const uint32_t lb = (uint32_t)((cnt * 4 + 15) & ~15);
     const long long ebeg = e0 + m0 * K;
-    if (KS == K) {
-      if (tid == 0) {
-        const uint32_t sb = (uint32_t)(((long long)cnt * K * 4 + 15) & ~15LL);
-        mbar_expect_tx(&bar[s], 3 * sb + lb);
-        bulk_g2s(st_var + s * L, var + ebeg, sb, &bar[s]);
-        bulk_g2s(st_exp + s * L, exps + ebeg, sb, &bar[s]);
-        bulk_g2s(st_dst + s * L, dst + ebeg, sb, &bar[s]);
-        bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
-      }
-      return;
-    }
-    const uint32_t rb = (uint32_t)K * 4;  // K % 4 == 0
-    if (tid == 0) {
-      mbar_expect_tx(&bar[s], 3 * cnt * rb + lb);
-      bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
-    }
-    __syncwarp();
-    for (int i = tid; i < 3 * cnt; i += 32) {
-      const int a = i / cnt, u = i - a * cnt;
-      const int32_t *src = (a == 0 ? var : a == 1 ? exps : dst) + ebeg + (long long)u * K;
-      int *d = (a == 0 ? st_var : a == 1 ? st_exp : st_dst) + s * L + u * KS;
-      bulk_g2s(d, src, rb, &bar[s]);
-    }
+    const uint32_t sb = (uint32_t)(((long long)cnt * K * 4 + 15) & ~15LL);
+    mbar_expect_tx(&bar[s], 3 * sb + lb);
+    bulk_g2s(st_var + s * L, var + ebeg, sb, &bar[s]);
+    bulk_g2s(st_exp + s * L, exps + ebeg, sb, &bar[s]);
+    bulk_g2s(st_dst + s * L, dst + ebeg, sb, &bar[s]);
+    bulk_g2s(st_lst + s * CH, list + m0, lb, &bar[s]);
   };
   long long ch = blockIdx.x;
-  if (ch < nchunks && tid < 32) issue(ch, 0);
+  if (ch < nchunks && tid == 0) issue(ch, 0);
   uint32_t phase[2] = {0, 0};
   for (int s = 0; ch < nchunks; ch += gridDim.x, s ^= 1) {
     const long long nxt = ch + gridDim.x;
-    if (nxt < nchunks && tid < 32) issue(nxt, s ^ 1);  // buffer s^1 was released by the last barrier
+    if (nxt < nchunks && tid == 0) issue(nxt, s ^ 1);  // buffer s^1 was released by the last barrier
     mbar_wait(&bar[s], phase[s]);
     phase[s] ^= 1;
     const long long m0 = ch * CH;
     const int u = tid / G, r = tid % G;
     const bool active = m0 + u < count;
     const int uu = active ? u : 0;
-    const int *mv = st_var + s * L + uu * KS;
-    const int *me = st_exp + s * L + uu * KS;
-    const int *md = st_dst + s * L + uu * KS;
+    const int *mv = st_var + s * L + uu * K;
+    const int *me = st_exp + s * L + uu * K;
+    const int *md = st_dst + s * L + uu * K;
     const int c = st_lst[s * CH + uu];
     const E co = eload<E>(coeff + (long long)c * es);
     mono_tree_eval<E, BASE, G>(
@@ -1000,16 +831,11 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
   const bool tma = tv ? strcmp(tv, "0") != 0 : Traits<E>::nc >= 2;
   if (b.dense_k && tma) {
     constexpr int CH = NT / G;
-    // PN_TREE_PAD=1: padded row stride KS = G (mod 32), rows copied one by
-    // one (16-byte rows).  Removes the 4-way bank conflicts of the support
-    // reads (ncu: 3.5e8 -> 3.9e6 on C5) but the per-row bulk copies cost more
-    // than the conflicts (C5 4158 -> 3900 start-iter/s, cqd eval 11.8 ->
-    // 12.2 ms), so the contiguous layout is the default.
-    const char *pv = getenv("PN_TREE_PAD");
-    int KS = b.dense_k;
-    if (pv && strcmp(pv, "1") == 0 && G % 4 == 0 && b.dense_k % 4 == 0)
-      while (KS % 32 != G % 32) ++KS;
-    const size_t smem = (size_t)(6 * CH * KS + 2 * CH) * sizeof(int);
+    // the chunk's supports arrive as one contiguous copy per array (padded
+    // rows, KS = G mod 32, removed the 4-way conflicts of the support reads
+    // but the per-row bulk copies cost more: C5 4158 -> 3900 start-iter/s,
+    // r01; removed)
+    const size_t smem = (size_t)(6 * CH * b.dense_k + 2 * CH) * sizeof(int);
     auto kern = k_mono_tree_tma<E, BASE, G, NT>;
     if constexpr (Traits<E>::nc >= 2 && BASE == 32) {
       // register cap for occupancy: qd 3 CTAs per SM (168 registers, cqd
@@ -1028,7 +854,7 @@ static void launch_tree(const pn_system::Bucket &b, pn_system *sys, const double
     const long long want = std::max(1LL, (long long)std::max(per_sm, 1) * num_sms() / std::max(nb, 1));
     const dim3 grid((unsigned)std::min(nchunks, want), (unsigned)nb);
     kern<<<grid, NT, smem, st>>>(b.d_list, b.count, b.dense_k, b.e0, sys->d_var, sys->d_exp, sys->d_dst, sys->d_coeff,
-                                 x, table, sys->d_toff, contrib, bv, KS, b.unit_exp);
+                                 x, table, sys->d_toff, contrib, bv, b.unit_exp);
     PN_CHECK_LAUNCH();
     count_launch(1);
     return;
@@ -1063,16 +889,6 @@ __global__ void k_zero_jac(long long count, double *__restrict__ A, BView bv) {
     a[i] = make_double2(0.0, 0.0);
 }
 
-// the fused path serves systems it was planned for (PN_EVAL_FUSED=1 at system
-// creation); PN_EVAL_FUSED=0 at call time turns it off again
-template <class E>
-static bool use_fused(const pn_system *sys, int nb, const BView &bv) {
-  if (!sys->fused.ok) return false;
-  const char *v = getenv("PN_EVAL_FUSED");
-  if (v && strcmp(v, "0") == 0) return false;
-  return fused_smem<E>(sys) <= 200 * 1024;
-}
-
 // the evaluation pipeline for nb slots (nb = 1, zero strides: one system)
 template <class E>
 static void evaldiff_run(pn_system *sys, const double *x, double *table, double *contrib, double *f, double *A,
@@ -1092,16 +908,6 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
       case 8: launch_rows<E, 8>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
       case 16: launch_rows<E, 16>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
       default: launch_rows<E, 32>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
-    }
-    return;
-  }
-  if (use_fused<E>(sys, nb, bv)) {
-    switch (sys->fused.base) {
-      case 2: launch_fused<E, 2>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
-      case 4: launch_fused<E, 4>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
-      case 8: launch_fused<E, 8>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
-      case 16: launch_fused<E, 16>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
-      default: launch_fused<E, 32>(sys, x, table, f, A, negf_col, nb, bv, consts, cstride, st); break;
     }
     return;
   }

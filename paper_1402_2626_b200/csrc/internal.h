@@ -122,7 +122,6 @@ struct MgsWork {
   DevArena status;  // MgsStatus
   DevArena ready;   // dataflow schedule: pivot-published flags (n+1 ints)
   DevArena own;     // flow schedule: column ownership table (G x maxo ints)
-  DevArena smslot;  // flow schedule: CTAs registered per SM id
   long long own_key = -1;
   int own_maxo = 0;
 };
@@ -220,17 +219,6 @@ struct pn_system {
   };
   std::vector<Bucket> buckets;
 
-  // plan of the fused evaluation (k_eval_fused): every monomial has k in
-  // {0, K}; chunks of 32 canonical monomials per polynomial; per support
-  // entry its slot in the chunk's (var, monomial)-sorted contribution list;
-  // per chunk the variable runs (var, start | len << 16)
-  struct Fused {
-    bool ok = false;
-    int K = 0, base = 0, D = 0;
-    long long nchunks = 0, nsegs = 0;
-    int16_t *d_ldst = nullptr;
-    int32_t *d_seg_var = nullptr, *d_seg_sl = nullptr, *d_chunk_seg = nullptr, *d_poly_chunk = nullptr;
-  } fused;
 
   // plan of the row evaluation (k_eval_rows): one CTA per polynomial at a
   // time, chunks of CH canonical monomials, per-variable binary-counter
@@ -265,6 +253,7 @@ struct pn_system {
   cudaGraphExec_t step_graph = nullptr;
   cudaStream_t graph_stream = nullptr;
   cudaEvent_t gev[5] = {};
+  cudaEvent_t pev[5] = {};  // phase events of the direct (non-graph) step
   long long graph_launches = 0;  // kernels inside the graph (launch counter)
   int graph_state = 0;
 

@@ -208,6 +208,21 @@ __device__ __forceinline__ void load_rows_cg(E (&v)[B], const double *__restrict
   }
 }
 
+// Intra-CTA step counter of the back-substitution lookahead: the solver
+// publishes x_j in shared memory and then the step count with a block-scope
+// release store; the lookahead group spins on an acquire load (libcu++
+// atomic_ref, so the ordering is explicit to the compiler and the tools).
+__device__ __forceinline__ void step_publish(int *step, int v) {
+  cuda::atomic_ref<int, cuda::thread_scope_block>(*step).store(v, cuda::memory_order_release);
+}
+__device__ __forceinline__ void step_wait(int *step, int above) {
+  cuda::atomic_ref<int, cuda::thread_scope_block> a(*step);
+  while (a.load(cuda::memory_order_acquire) <= above) __nanosleep(20);
+}
+__device__ __forceinline__ void step_reset(int *step) {
+  cuda::atomic_ref<int, cuda::thread_scope_block>(*step).store(0, cuda::memory_order_relaxed);
+}
+
 // publish pivot k: make this CTA's Q/R writes visible, then raise the flag
 // diagnostics (PN_MGS_TRACE=file): global-timer stamp of every published pivot
 __device__ unsigned long long *g_mgs_trace = nullptr;
@@ -466,8 +481,7 @@ template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
                                                     MgsStatus *status, int *ready, int kstop, int hold, int lag,
-                                                    const int *__restrict__ own, int maxo, int pickrule,
-                                                    int *smslot, int S) {
+                                                    const int *__restrict__ own, int maxo, int pickrule) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
@@ -484,36 +498,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
   const int lane = tid & 31, w = tid >> 5;
   const int row0 = tid * B;
   const int nparts = (m + B - 1) / B;
-  // Which table row this CTA takes.  With smslot, rows follow the SM the
-  // CTA actually runs on (row = dense SM rank + S * slot on that SM), so the
-  // SM-level schedule of the table holds whatever the block scheduler did;
-  // if the placement is not exactly two CTAs on each of S SMs, every CTA
-  // falls back to its block index (the same decision everywhere).
-  int row = cta;
-  if (smslot) {
-    __shared__ int s_row;
-    unsigned smid, nsm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-    int slot = 0;
-    if (tid == 0) slot = atomicAdd(smslot + smid, 1);
-    cooperative_groups::this_grid().sync();
-    if (tid == 0) {
-      int rank = 0, used = 0;
-      bool even = true;
-      for (unsigned i = 0; i < nsm && i < 1024; ++i) {
-        const int c = ld_acquire(smslot + i);
-        if (c) {
-          ++used;
-          even &= c == 2;
-          if (i < smid) ++rank;
-        }
-      }
-      s_row = (even && used == S) ? rank + S * slot : cta;
-    }
-    __syncthreads();
-    row = s_row;
-  }
+  const int row = cta;  // the CTA's row of the ownership table
   // the CTA's columns, ascending (own: maxo per CTA, -1 padded)
   int cols[64];
   int nown = 0;
@@ -749,7 +734,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
 // pairwise order (the top levels), so r_kj, the norms and therefore Q and R
 // stay bit-identical.  Pivot j is published when all S parts have stored
 // their rows of q_j (ready[j] counts to S).
-template <class E, int B, int NT, bool CL = false>
+template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ A, int m, int n, const double *__restrict__ orig,
                                                  double eps, double *__restrict__ Q, double *__restrict__ R,
                                                  MgsStatus *status, int *ready, int kstop, int S,
@@ -778,36 +763,9 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
   // exchange slot of column ci: [2 parity][S] elements (E units) + flags
   E *xe = reinterpret_cast<E *>(xch) + (long long)ci * 2 * S;
   int *xf = xflag + (long long)ci * 2 * S;
-  // CL: the S parts of a column form a thread-block cluster and exchange
-  // through distributed shared memory: each part leaves its partial in its
-  // own shared slot (parity-double-buffered like the global slots), one
-  // cluster barrier, thread 0 reads the S slots of the cluster.  A slot is
-  // rewritten two exchanges later, after every peer has passed the barrier
-  // that follows its read.
-  __shared__ __align__(16) double s_xch[2][es];
-  auto cl_sync = [&]() {
-    if constexpr (CL) cooperative_groups::this_cluster().sync();
-  };
   // publish this part's partial with tag, gather all S, combine in tree order
   auto exchange = [&](auto v, int tag) {
     using T = decltype(v);
-    if constexpr (CL) {
-      namespace cg = cooperative_groups;
-      cg::cluster_group cl = cg::this_cluster();
-      T *mine = reinterpret_cast<T *>(s_xch[tag & 1]);
-      if (tid == 0) *mine = v;
-      cl.sync();
-      T acc = v;
-      if (tid == 0) {
-        T w[8];
-        for (int p = 0; p < sparts; ++p) w[p] = *cl.map_shared_rank(mine, p);
-        for (int st = 1; st < sparts; st <<= 1)
-          for (int p = 0; p + st < sparts; p += 2 * st) w[p] = eadd(w[p], w[p + st]);
-        acc = w[0];
-        s_ok = 1;
-      }
-      return acc;
-    }
     T *slot = reinterpret_cast<T *>(xe + (tag & 1) * S);
     if (tid == 0) {
       slot[part] = v;
@@ -855,10 +813,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
         s_ok = ok;
       }
       __syncthreads();
-      if (!s_ok) {  // every part of a column waits on the same flag: all leave here
-        cl_sync();
-        return;
-      }
+      if (!s_ok) return;  // every part of a column waits on the same flag: all leave here
       const double *qk = Q + (long long)k * m * es;
       E qv[B];
 #pragma unroll
@@ -899,7 +854,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
           __threadfence();
           atomicExch(&status->code, PN_E_BREAKDOWN);
         }
-        cl_sync();  // the peers may still read this CTA's exchange slot
         return;
       }
     }
@@ -913,144 +867,6 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
       __syncthreads();
       if (tid == 0) red_release_add(ready + j, 1);
     }
-  }
-  cl_sync();  // keep the exchange slots alive until every peer has read them
-}
-
-// ---------------------------------------------------------------------------
-// k_mgs_warp: the latency-bound levels (d, dd) at m <= 32*R.  One warp per
-// column (one-warp CTAs, cooperative launch so every column owner is
-// resident).  Lane l owns the aligned row block [l*R, l*R+R) of its column,
-// kept in shared memory (interleaved: row l*R+i at i*32+l, bank-conflict
-// free), so a sweep is R products per lane, a pairwise tree over the block,
-// and a warp shuffle tree over the lanes (tree_sum's order) --
-// no CTA barriers anywhere on the critical path.  The owner of column k+1
-// sees q_k through an acquire poll, applies sweep k, normalises and
-// publishes q_{k+1}; every other column catches up on its own.  The
-// operation sequence per column is the reference's, so results are
-// bit-identical to the other schedules.
-// pairwise tree (binary counter) over a lane's R-row block, row i supplied
-// by f(i) for i < valid: full blocks (the common case) resolve every level
-// at compile time and stay in registers
-constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
-template <class E, int R, class Fn>
-__device__ __forceinline__ E block_pairwise(int valid, Fn &&f) {
-  constexpr int L = ilog2(R);
-  if (valid == R) {
-    E st[L + 1];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      E v = f(i);
-#pragma unroll
-      for (int l = 0; l <= L; ++l) {
-        if (!((i >> l) & 1)) {
-          st[l] = v;
-          break;
-        }
-        v = eadd(st[l], v);
-      }
-    }
-    return st[L];
-  }
-  Pairwise<E, L + 1> pw;
-  for (int i = 0; i < valid; ++i) pw.push(f(i));
-  return valid > 0 ? pw.fold() : ezero<E>();
-}
-
-template <class E, int R>
-__global__ void __launch_bounds__(32) k_mgs_warp(double *__restrict__ A, int m, int n, double eps,
-                                                 double *__restrict__ Q, double *__restrict__ Rm,
-                                                 MgsStatus *status, int *ready) {
-  using Rl = typename Traits<E>::R;
-  constexpr int es = Traits<E>::es;
-  extern __shared__ __align__(16) double wcol[];  // es planes x (R*32)
-  const int j = blockIdx.x;
-  if (j > n) return;
-  const int lane = threadIdx.x;
-  const int row0 = lane * R;
-  const int nparts = (m + R - 1) / R;
-  const int valid = m - row0 <= 0 ? 0 : (m - row0 >= R ? R : m - row0);
-  auto cget = [&](int i) -> E {
-    E v;
-    double *d = reinterpret_cast<double *>(&v);
-#pragma unroll
-    for (int c = 0; c < es; ++c) d[c] = wcol[c * (R * 32) + i * 32 + lane];
-    return v;
-  };
-  auto cput = [&](int i, const E &v) {
-    const double *d = reinterpret_cast<const double *>(&v);
-#pragma unroll
-    for (int c = 0; c < es; ++c) wcol[c * (R * 32) + i * 32 + lane] = d[c];
-  };
-  // warp tree over the lanes' block partials (absorb rule, right-pruned)
-  auto warp_tree = [&](auto v) {
-#pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      const auto o = eshfl_down(v, s);
-      if ((lane & (2 * s - 1)) == 0 && lane + s < nparts) v = eadd(v, o);
-    }
-    return eshfl_idx(v, 0);
-  };
-  auto norm = [&]() -> Rl {
-    return fsqrt(warp_tree(block_pairwise<Rl, R>(valid, [&](int i) { return eabs2(cget(i)); })));
-  };
-  const double *col = A + (long long)j * m * es;
-#pragma unroll
-  for (int i = 0; i < R; ++i) cput(i, row0 + i < m ? eload<E>(col + (long long)(row0 + i) * es) : ezero<E>());
-  // original norm (mgs.py:171-172): only this column's owner needs it
-  const double orig = norm().c[0];
-  const long long ldR = n + 1;
-  for (int k = 0; k < j; ++k) {
-    // wait for pivot k: lane 0 polls, then every lane acquires once
-    if (lane == 0) {
-      long long t0 = clock64();
-      while (ld_acquire(ready + k) == 0) {
-        if (ld_acquire(&status->code) != 0) break;
-        __nanosleep(100);
-        if (clock64() - t0 > (1ll << 36)) {
-          status->k = k;
-          atomicExch(&status->code, PN_E_CUDA);
-          break;
-        }
-      }
-    }
-    __syncwarp();
-    if (ld_acquire(ready + k) == 0 || ld_acquire(&status->code) != 0) return;
-    const double *qk = Q + (long long)k * m * es;
-    E qv[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) qv[i] = row0 + i < m ? eload_cg<E>(qk + (long long)(row0 + i) * es) : ezero<E>();
-    const E rk = warp_tree(block_pairwise<E, R>(valid, [&](int i) { return emul(econj(qv[i]), cget(i)); }));
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (row0 + i < m) cput(i, esub(cget(i), emul(qv[i], rk)));
-    if (lane == 0) estore(Rm + ((long long)j * ldR + k) * es, rk);
-  }
-  // pivot j (mgs.py:176-193); j == n is the residual norm z
-  const Rl rkk = norm();
-  if (j < n) {
-    const double thr = __dmul_rn(__dmul_rn(__dmul_rn(1.0, (double)n), eps), orig);
-    if (rkk.c[0] <= thr) {
-      if (lane == 0) {
-        status->k = j;
-        status->rkk = rkk.c[0];
-        status->thr = thr;
-        __threadfence();
-        atomicExch(&status->code, PN_E_BREAKDOWN);
-      }
-      return;
-    }
-  }
-  if (lane == 0) estore(Rm + ((long long)j * ldR + j) * es, eembed(rkk, (E *)nullptr));
-  if (j < n) {
-    const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
-    double *qc = Q + (long long)j * m * es;
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (row0 + i < m) estore(qc + (long long)(row0 + i) * es, ediv_prepared(cget(i), p));
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(ready + j, 1);
   }
 }
 
@@ -1301,7 +1117,8 @@ static double level_eps(int nc) { return nc == 1 ? 0x1p-53 : nc == 2 ? 0x1p-104 
 
 // PN_MGS_MODE=sweeps selects the launch-per-sweep schedule (kept as the
 // reference schedule for tests); the default is the persistent dataflow kernel.
-// 0 flow, 1 dataflow, 2 sweeps, 3 warp, 4 pipe.  Default by measurement
+// 0 flow, 1 dataflow, 2 sweeps, 4 pipe, 5 small (the warp-per-column
+// schedule, 2-3x slower for cd/cdd in r01, was removed).  Default by measurement
 // (profiles/r01): the priority/smem schedule wins when sweeps are
 // compute-heavy (quad double); for d/dd the TMA-pipelined dataflow kernel
 // (k_mgs_pipe, m a multiple of 256 up to 1024) and otherwise the plain
@@ -1311,31 +1128,9 @@ static int mgs_mode(int nc) {
   if (v && strcmp(v, "sweeps") == 0) return 2;
   if (v && strcmp(v, "dataflow") == 0) return 1;
   if (v && strcmp(v, "flow") == 0) return 0;
-  if (v && strcmp(v, "warp") == 0) return 3;
   if (v && strcmp(v, "pipe") == 0) return 4;
   if (v && strcmp(v, "small") == 0) return 5;
   return nc == 4 ? 0 : 4;
-}
-
-// warp-per-column schedule when every column owner fits on the GPU at once
-template <class E, int R>
-static bool try_mgs_warp(int m, int n, double *A, double *Q, double *R_, MgsWork &w, cudaStream_t st) {
-  constexpr int es = Traits<E>::es;
-  const size_t smem = (size_t)es * R * 32 * sizeof(double);
-  auto kern = k_mgs_warp<E, R>;
-  if (smem > 48 * 1024) PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem));
-  if ((long long)per_sm * num_sms() < n + 1) return false;
-  MgsStatus *status = w.status.as<MgsStatus>();
-  w.ready.ensure((size_t)(n + 1) * sizeof(int));
-  PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
-  int *ready = w.ready.as<int>();
-  const double eps = level_eps(Traits<E>::nc);
-  void *args[] = {&A, &m, &n, (void *)&eps, &Q, &R_, &status, &ready};
-  PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, n + 1, 32, args, smem, st));
-  count_launch(1);
-  return true;
 }
 
 static void trace_begin(int n, unsigned long long **buf) {
@@ -1370,37 +1165,16 @@ static void trace_end(int n, unsigned long long *buf, cudaStream_t st) {
 // "snake": CTA-level alternating direction (pivot n-C 14 ms sooner but the
 // tail kernel's columns are left behind: +4 ms).  Other in-SM splits
 // (greedy by load, ABBA) were slower (scripts/own/*.txt, profiles/r01).
-// PN_FLOW_OWN=smsnake|rr|snake|<file> (file: one line per CTA, its columns).
+// PN_FLOW_OWN=smsnake|rr|snake.
 static void flow_owner_table(int n, int G, MgsWork &w, cudaStream_t st) {
   const char *v = getenv("PN_FLOW_OWN");
   const int S = num_sms();
   const bool pairs = G == 2 * S;  // two CTAs per SM: c and c + S share one
-  const int var = !v ? (pairs ? 3 : 0)
-                     : strcmp(v, "rr") == 0 ? 0
-                     : strcmp(v, "snake") == 0 ? 1
-                     : strcmp(v, "smsnake") == 0 ? (pairs ? 3 : 0) : 2;
+  const int var = v && strcmp(v, "rr") == 0 ? 0 : v && strcmp(v, "snake") == 0 ? 1 : (pairs ? 3 : 0);
   const long long key = ((long long)n << 32) | ((long long)G << 4) | var;
-  if (w.own_key == key && var != 2) return;
+  if (w.own_key == key) return;
   std::vector<std::vector<int>> lists(G);
-  if (var == 2) {
-    FILE *fp = fopen(v, "r");
-    if (!fp) {
-      set_error("PN_FLOW_OWN: cannot open %s", v);
-      throw Fail{PN_E_ARG};
-    }
-    char line[8192];
-    for (int c = 0; c < G && fgets(line, sizeof line, fp); ++c) {
-      char *q = line;
-      for (;;) {
-        char *e = nullptr;
-        const long j = strtol(q, &e, 10);
-        if (e == q) break;
-        if (j >= 0 && j <= n) lists[c].push_back((int)j);
-        q = e;
-      }
-    }
-    fclose(fp);
-  } else if (var == 3) {
+  if (var == 3) {
     // SM-level snake: round r of S columns goes to SMs 0..S-1, alternating
     // direction; an SM's r-th column goes to its CTA s (r even) or s + S
     for (int j = 0; j <= n; ++j) {
@@ -1452,41 +1226,18 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
   const int grid = std::min(per_sm * num_sms(), n + 1);
   if (per_sm <= 0 || (n + 1 + grid - 1) / grid > 64) return false;
-  // row-split tail (quad double): the last C columns, S CTAs each; parts of
-  // RQ = 256 rows by default (see the variants below)
-  // variants: "a" = 128 threads x 2 rows (4 CTAs/SM), "b" = 64 threads x 4
-  // rows (8 CTAs/SM, twice the columns), "c" = 128 x 4 (512-row parts)
+  // row-split tail (quad double): the last C columns, S CTAs each, parts of
+  // RQ = 256 rows (128 threads x 2 rows, four CTAs per SM; 64 x 4 and
+  // 128 x 4-row variants and a cluster/DSMEM exchange were measured slower
+  // or equal in r01 and removed)
   const char *tv = getenv("PN_MGS_TAIL");
-  const char *vv = getenv("PN_MGS_TAIL_VARIANT");
-  const char var = vv && *vv ? vv[0] : 'a';
   const void *tk = (const void *)k_mgs_tail<E, 2, 128>;
-  int tnt = 128, RQ = 256;
-  if (var == 'b') { tk = (const void *)k_mgs_tail<E, 4, 64>; tnt = 64; RQ = 256; }
-  if (var == 'c') { tk = (const void *)k_mgs_tail<E, 4, 128>; tnt = 128; RQ = 512; }
+  const int tnt = 128, RQ = 256;
   int kstop = n + 1, S = (m + RQ - 1) / RQ, C = 0;
   if (Traits<E>::nc == 4 && S >= 2 && S <= 8 && !(tv && strcmp(tv, "0") == 0)) {
     int tper = 0;
     PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, tk, tnt, 0));
     C = std::min(n + 1, tper * num_sms() / S);
-    const char *cv0 = getenv("PN_MGS_TAIL_CLUSTER");
-    if (cv0 && strcmp(cv0, "1") == 0 && var == 'a') {
-      // clusters of S CTAs must fit inside a GPC: fewer columns co-reside
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(S);
-      cfg.blockDim = dim3(tnt);
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = S;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, (const void *)k_mgs_tail<E, 2, 128, true>, &cfg) == cudaSuccess)
-        C = std::min(C, ncl);
-      else
-        cudaGetLastError();
-    }
     if (tv && atoi(tv) > 0) C = std::min(C, atoi(tv));
     if (C >= 16) kstop = n + 1 - C;
     else C = 0;
@@ -1508,19 +1259,7 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   // cqd MGS 107.5 -> 106.8 ms), 0 = lowest index (earliest deadline)
   const char *pv = getenv("PN_FLOW_PICK");
   int pickrule = pv ? atoi(pv) : 1;
-  // PN_FLOW_SMMAP=1: table rows by the SM a CTA lands on instead of the
-  // block index (guards the SM pairing c / c + S the smsnake table assumes;
-  // measured 1 ms slower than the block-index rows, which already pair up)
-  const char *mv = getenv("PN_FLOW_SMMAP");
-  int *smslot = nullptr;
-  int nsms = num_sms();
-  if (grid == 2 * nsms && mv && strcmp(mv, "1") == 0) {
-    w.smslot.ensure(1024 * sizeof(int));
-    PN_CHECK_CUDA(cudaMemsetAsync(w.smslot.p, 0, 1024 * sizeof(int), st));
-    smslot = w.smslot.as<int>();
-  }
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule,
-                  &smslot, &nsms};
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
@@ -1532,34 +1271,7 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
     double *xp = xch.d();
     int *xf = xfl.as<int>();
     void *targs[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &S, &xp, &xf};
-    // PN_MGS_TAIL_CLUSTER=1: the S parts of a column as one thread-block
-    // cluster exchanging through distributed shared memory (variant a)
-    const char *cv = getenv("PN_MGS_TAIL_CLUSTER");
-    bool launched = false;
-    if (cv && strcmp(cv, "1") == 0 && var == 'a') {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(C * S);
-      cfg.blockDim = dim3(tnt);
-      cfg.stream = st;
-      cudaLaunchAttribute at[2];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = S;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      at[1].id = cudaLaunchAttributeCooperative;
-      at[1].val.cooperative = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 2;
-      const cudaError_t le = cudaLaunchKernelExC(&cfg, (const void *)k_mgs_tail<E, 2, 128, true>, targs);
-      launched = le == cudaSuccess;
-      if (!launched) {
-        cudaGetLastError();
-        static bool told = false;
-        if (!told) fprintf(stderr, "k_mgs_tail cluster launch refused (%s); plain launch\n", cudaGetErrorName(le));
-        told = true;
-      }
-    }
-    if (!launched) PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, tnt, targs, 0, st));
+    PN_CHECK_CUDA(cudaLaunchCooperativeKernel(tk, C * S, tnt, targs, 0, st));
     count_launch(1);
   }
   trace_end(n, tr, st);
@@ -1706,14 +1418,6 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     return;
   }
   if (mode == 5) mode = Traits<E>::nc == 4 ? 0 : 4;
-  if (mode == 3 && Traits<E>::nc <= 2 && m <= 1024) {
-    bool done = false;
-    if (m <= 128) done = try_mgs_warp<E, 4>(m, n, A, Q, R, w, st);
-    else if (m <= 256) done = try_mgs_warp<E, 8>(m, n, A, Q, R, w, st);
-    else if (m <= 512) done = try_mgs_warp<E, 16>(m, n, A, Q, R, w, st);
-    else done = try_mgs_warp<E, 32>(m, n, A, Q, R, w, st);
-    if (done) return;
-  }
   if (mode == 4 && Traits<E>::nc <= 2 && m % 256 == 0 && m <= 1024) {
     bool done = false;
     switch (m / 256) {
@@ -1729,11 +1433,6 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     // a 96 KB column, two CTAs per SM instead of one 128 KB CTA
     if constexpr (B == 8) {
       if (m <= 1536 && flow_launch<E, B, 192>(m, n, A, Q, R, w, st)) return;
-    }
-    // PN_FLOW_NT=128: 4 warps x 8 rows, three CTAs per SM (m <= 1024)
-    if constexpr (B == 4) {
-      const char *fv = getenv("PN_FLOW_NT");
-      if (fv && atoi(fv) == 128 && flow_launch<E, 8, 128>(m, n, A, Q, R, w, st)) return;
     }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
@@ -2081,7 +1780,7 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
   __shared__ int s_step[1];  // solver steps whose x_j is in sX
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;
-  if (threadIdx.x == 0) s_step[0] = 0;
+  if (threadIdx.x == 0) step_reset(s_step);
   const long long ld = n + 1;
   const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
   for (int j = gtid; j < n; j += gsize) {
@@ -2152,8 +1851,7 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
             const E xj = lp_div(yr, sD[jl * 32 + jl], sP[jl], p, g4);
             if (rl == jl && p == 0) {
               sX[par * 32 + jl] = xj;
-              __threadfence_block();
-              *(volatile int *)s_step = s + 1;
+              step_publish(s_step, s + 1);
             }
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -2166,14 +1864,13 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
         // block b+1's x first, then block b's as the solver publishes them
         while (q < ncu) look();
         for (int s = 0; s < nbk; ++s) {
-          while (*(volatile int *)s_step <= s) __nanosleep(20);
-          __threadfence_block();
+          step_wait(s_step, s);
           look();
         }
         if (p == 0) sY[rl] = v;
       }
       __syncthreads();
-      if (t == 0) *(volatile int *)s_step = 0;
+      if (t == 0) step_reset(s_step);
       if (solver && tt < nbk) estore(x + (long long)(lo + tt) * es, sX[par * 32 + tt]);
     } else if (b + 1 < nb) {
       // rows below block b-1 take block b+1's x (descending columns)
@@ -2214,7 +1911,7 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
   __shared__ int s_step[1];
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;
-  if (threadIdx.x == 0) s_step[0] = 0;
+  if (threadIdx.x == 0) step_reset(s_step);
   const long long ld = n + 1;
   const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
   for (int j = gtid; j < n; j += gsize) {
@@ -2260,8 +1957,7 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
           if (lane == jl) {
             xl = ediv_with(yr, sD[jl * 32 + jl], sP[jl]);
             sX[par * 32 + jl] = xl;
-            __threadfence_block();
-            *(volatile int *)s_step = s + 1;
+            step_publish(s_step, s + 1);
           }
           const E xj = eshfl_idx(xl, jl);
           if (lane < jl) yr = esub(yr, emul(sD[jl * 32 + lane], xj));
@@ -2272,14 +1968,13 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
         for (int jj = ncu - 1; jj >= 0; --jj) v = esub(v, emul(sV[jj * 32 + lane], sX[(par ^ 1) * 32 + jj]));
         for (int s = 0; s < nbk; ++s) {
           const int jl = nbk - 1 - s;
-          while (*(volatile int *)s_step <= s) __nanosleep(20);
-          __threadfence_block();
+          step_wait(s_step, s);
           v = esub(v, emul(sU[jl * 32 + lane], sX[par * 32 + jl]));
         }
         sY[lane] = v;
       }
       __syncthreads();
-      if (threadIdx.x == 0) *(volatile int *)s_step = 0;
+      if (threadIdx.x == 0) step_reset(s_step);
     } else if (b + 1 < nb) {
       const int c0 = lo + 32, nc1 = min(n, lo + 64) - c0;
       for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {

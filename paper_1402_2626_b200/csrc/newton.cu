@@ -78,14 +78,10 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
   double *xa = sys->xbuf.d(), *A = sys->Abuf.d(), *fa = sys->fbuf.d();
   double *Q = sys->vbuf.d(), *R = sys->Rbuf.d(), *dxa = sys->xsol.d(), *xn = dxa + (size_t)n * es;
 
-  cudaEvent_t evl[5];
-  for (auto &e : evl) PN_CHECK_CUDA(cudaEventCreate(&e));
-  struct EvGuard {
-    cudaEvent_t *e;
-    ~EvGuard() {
-      for (int i = 0; i < 5; ++i) cudaEventDestroy(e[i]);
-    }
-  } guard{evl};
+  // phase events: created once per system and reused by every step
+  if (!sys->pev[0])
+    for (auto &e : sys->pev) PN_CHECK_CUDA(cudaEventCreate(&e));
+  cudaEvent_t *evl = sys->pev;
   // the device step from x (AoS in xa) to x_next; `external` records the
   // phase events as graph nodes visible outside the graph
   auto device_step = [&](cudaStream_t s, cudaEvent_t *e, bool external) {

@@ -31,11 +31,6 @@ pn_system::~pn_system() {
   cudaFree(d_seg_ptr);
   cudaFree(d_seg_out);
   for (auto &b : buckets) cudaFree(b.d_list);
-  cudaFree(fused.d_ldst);
-  cudaFree(fused.d_seg_var);
-  cudaFree(fused.d_seg_sl);
-  cudaFree(fused.d_chunk_seg);
-  cudaFree(fused.d_poly_chunk);
   cudaFree(rows.d_ent);
   cudaFree(rows.d_poly_chunk);
   cudaFree(rows.d_desc);
@@ -43,6 +38,8 @@ pn_system::~pn_system() {
   if (ev) cudaEventDestroy(ev);
   if (step_graph) cudaGraphExecDestroy(step_graph);
   for (auto e : gev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : pev)
     if (e) cudaEventDestroy(e);
   if (graph_stream) cudaStreamDestroy(graph_stream);
 }
@@ -86,82 +83,6 @@ inline int floor_pow2(int k) {
   while (b * 2 <= k) b *= 2;
   return b;
 }
-
-// Plan of the fused evaluation kernel (evaldiff.cu, k_eval_fused): eligible
-// when every monomial has k in {0, K} with 2 <= K <= 32 and the per-variable
-// stacks of one polynomial (n x D elements, D = bit length of the longest
-// Jacobian-entry run) fit in shared memory.  Chunks are 32 consecutive
-// canonical monomials of a polynomial; inside a chunk the support entries are
-// ranked by (variable, monomial), which is the reference's summation order
-// restricted to the chunk (evaldiff.py:252-265).
-void build_fused_plan(pn_system &S, const int32_t *poly_ptr, const std::vector<int32_t> &cptr,
-                      const std::vector<int32_t> &cvar) {
-  // opt-in (PN_EVAL_FUSED=1 when the system is created): measured slower
-  // than K1 + K2 on C5 (45.9 vs 24.1 + 7.5 ms per 296 starts, profiles/r01)
-  // because the per-variable pushes of a chunk diverge across lanes
-  const char *env = getenv("PN_EVAL_FUSED");
-  if (!(env && strcmp(env, "1") == 0)) return;
-  const int m = S.m, n = S.n;
-  constexpr int CH = 32;
-  int K = -1;
-  for (int64_t c = 0; c < S.M; ++c) {
-    const int k = cptr[c + 1] - cptr[c];
-    if (k == 0) continue;
-    if (K < 0) K = k;
-    else if (k != K) return;
-  }
-  if (K < 2 || K > 32) return;
-  std::vector<int32_t> L(n, 0);
-  int maxL = 0;
-  for (int i = 0; i < m; ++i) {
-    for (int32_t t = cptr[poly_ptr[i]]; t < cptr[poly_ptr[i + 1]]; ++t) maxL = std::max(maxL, ++L[cvar[t]]);
-    for (int32_t t = cptr[poly_ptr[i]]; t < cptr[poly_ptr[i + 1]]; ++t) L[cvar[t]] = 0;
-  }
-  int D = 1;
-  while ((1 << D) <= maxL) ++D;
-  if ((size_t)n * D * S.es * 8 > 160 * 1024) return;
-  std::vector<int16_t> ldst(S.nnz);
-  std::vector<int32_t> seg_var, seg_sl, chunk_seg{0}, poly_chunk{0};
-  std::vector<std::pair<int64_t, int32_t>> keys;
-  for (int i = 0; i < m; ++i) {
-    const int T = poly_ptr[i + 1] - poly_ptr[i];
-    const int nch = (T + CH - 1) / CH;
-    for (int ch = 0; ch < nch; ++ch) {
-      const int64_t cm0 = poly_ptr[i] + (int64_t)ch * CH;
-      const int U = std::min(CH, T - ch * CH);
-      keys.clear();
-      for (int u = 0; u < U; ++u)
-        for (int32_t t = cptr[cm0 + u]; t < cptr[cm0 + u + 1]; ++t) keys.push_back({(int64_t)cvar[t] * CH + u, t});
-      std::sort(keys.begin(), keys.end());
-      for (size_t r = 0; r < keys.size();) {
-        size_t q = r;
-        const int64_t v = keys[r].first / CH;
-        while (q < keys.size() && keys[q].first / CH == v) {
-          ldst[keys[q].second] = (int16_t)q;
-          ++q;
-        }
-        seg_var.push_back((int32_t)v);
-        seg_sl.push_back((int32_t)(r | ((q - r) << 16)));
-        r = q;
-      }
-      chunk_seg.push_back((int32_t)seg_var.size());
-    }
-    poly_chunk.push_back(poly_chunk.back() + nch);
-  }
-  auto &F = S.fused;
-  F.K = K;
-  F.base = floor_pow2(K);
-  F.D = D;
-  F.nchunks = (long long)chunk_seg.size() - 1;
-  F.nsegs = (long long)seg_var.size();
-  F.d_ldst = upload(ldst);
-  F.d_seg_var = upload(seg_var);
-  F.d_seg_sl = upload(seg_sl);
-  F.d_chunk_seg = upload(chunk_seg);
-  F.d_poly_chunk = upload(poly_chunk);
-  F.ok = true;
-}
-
 
 // Plan of the row evaluation (evaldiff.cu, k_eval_rows).  Eligible when
 // every non-constant monomial has the same k = K (2 <= K <= 32), n fits 16
@@ -446,7 +367,6 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
   S.d_tdeg = upload(tdeg);
   S.d_seg_ptr = upload(seg_ptr);
   S.d_seg_out = upload(seg_out);
-  build_fused_plan(S, poly_ptr, cptr, cvar);
   build_rows_plan(S, poly_ptr, cptr, cvar, cexp);
   PN_CHECK_CUDA(cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
   *out = sys.release();

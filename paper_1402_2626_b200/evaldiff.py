@@ -129,13 +129,26 @@ class SystemEvaluation:
         return self._jacobian
 
 
-def point_planes(point, level: PrecisionLevel) -> np.ndarray:
-    """A point (list of scalars or a planes array) as contiguous planes."""
+def point_planes(point, level: PrecisionLevel, n: int | None = None, batch: int | None = None) -> np.ndarray:
+    """A point (list of scalars or a planes array / torch tensor) as
+    contiguous float64 planes of shape level.cshape + (n,) -- or
+    level.cshape + (batch, n) for a batch of points.  The C ABI reads exactly
+    that many doubles from the pointer, so a wrong shape or dtype is refused
+    here (ValueError) instead of reading past the end of the buffer."""
     if isinstance(point, np.ndarray):
-        return np.ascontiguousarray(point, dtype=np.float64)
-    if hasattr(point, "data_ptr"):
-        return point
-    return level.to_planes(list(point))
+        x = np.ascontiguousarray(point, dtype=np.float64)
+    elif hasattr(point, "data_ptr"):
+        import torch
+        if point.dtype != torch.float64 or not point.is_contiguous():
+            raise ValueError("point tensor must be contiguous float64 planes")
+        x = point
+    else:
+        x = level.to_planes(list(point))
+    want = tuple(level.cshape) + (() if batch is None else (batch,)) + (() if n is None else (n,))
+    got = tuple(x.shape)
+    if n is not None and (len(got) != len(want) or got != want):
+        raise ValueError(f"point planes have shape {got}, expected {want} for this system and precision")
+    return x
 
 
 def evaluate_system(system, point, counter: OpCounter | None = None,
@@ -148,9 +161,9 @@ def evaluate_system(system, point, counter: OpCounter | None = None,
     prep = system if isinstance(system, PreparedSystem) else PreparedSystem(system)
     level = prep.level
     n = prep.n_vars
-    x = point_planes(point, level)
-    if x.shape[-1] != n:
-        raise ValueError(f"point dimension {x.shape[-1]} != n_vars {n}")
+    if isinstance(point, (list, tuple)) and len(point) != n:
+        raise ValueError(f"point dimension {len(point)} != n_vars {n}")
+    x = point_planes(point, level, n)
     m = prep.n_eqs
     f = np.empty(level.cshape + (m,))
     J = np.empty(level.cshape + (m, n))

@@ -121,7 +121,7 @@ def device_step(prep: PreparedSystem, x) -> StepResult:
     """One fused GPU Newton step on planes (host or device arrays)."""
     level = prep.level
     m, n = prep.n_eqs, prep.n_vars
-    xp = point_planes(x, level)
+    xp = point_planes(x, level, n)
     x_next = np.empty(level.cshape + (n,))
     f = np.empty(level.cshape + (m,))
     dx = np.empty(level.cshape + (n,))

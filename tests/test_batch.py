@@ -56,6 +56,57 @@ def test_gather_batch_gloo_world2(tmp_path, B):
         assert np.array_equal(d["status"], np.arange(B) % 3)
 
 
+def _run_batched_worker(rank, world, port, B, out_dir):
+    """run_batched's shard -> solve -> gather with stub prepare/solve: every
+    rank must solve exactly its shard_range and end with the full batch."""
+    import torch.distributed as dist
+    from paper_1402_2626_b200.batch import BatchResult, run_batched
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    n = 4
+    Z = np.zeros((2, 2, B, n))
+    Z[0, 0] = np.arange(B)[:, None] + 0.25 * np.arange(n)
+    seen = {}
+
+    def prepare(packed, Zs, t):
+        seen["prepared"] = Zs.shape[-2]
+        return "prep", Zs[..., 0] * t  # per-start stand-in for the homotopy constants
+
+    def solve(prep, Zs, consts, max_iters, tol):
+        assert prep == "prep" and consts.shape[-1] == Zs.shape[-2]
+        start = Zs[0, 0, :, 0].astype(int)   # each start carries its global index
+        x = Zs * 2.0 + 1.0
+        return BatchResult(x, (start % max_iters).astype(np.int32), (start % 4).astype(np.int32))
+
+    shard, full, (lo, hi) = run_batched(None, Z, 3.0, max_iters=5, prepare=prepare, solve=solve)
+    np.savez(os.path.join(out_dir, f"rb{rank}.npz"), x=full.x, iters=full.iters, status=full.status,
+             lo=lo, hi=hi, prepared=seen["prepared"], shard_n=shard.x.shape[-2])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [7, 8192])
+def test_run_batched_orchestration_gloo_world2(tmp_path, B):
+    import socket
+
+    import torch.multiprocessing as mp
+    from paper_1402_2626_b200.batch import shard_range
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_run_batched_worker, args=(2, port, B, str(tmp_path)), nprocs=2, join=True)
+    n = 4
+    Z = np.zeros((2, 2, B, n))
+    Z[0, 0] = np.arange(B)[:, None] + 0.25 * np.arange(n)
+    for r in range(2):
+        d = np.load(tmp_path / f"rb{r}.npz")
+        lo, hi = shard_range(B, 2, r)
+        assert (int(d["lo"]), int(d["hi"])) == (lo, hi)
+        assert int(d["prepared"]) == hi - lo == int(d["shard_n"])
+        assert np.array_equal(d["x"], Z * 2.0 + 1.0)
+        assert np.array_equal(d["iters"], np.arange(B) % 5)
+        assert np.array_equal(d["status"], np.arange(B) % 4)
+
+
 # -- GPU ---------------------------------------------------------------------------------
 
 def _packed(g, prefix=""):

@@ -65,28 +65,3 @@ def test_flow_schedules_bit_identical(gpu, case, own, hold, pick):
         _check(_solve(aug), ref)
 
 
-def test_flow_rows_by_sm(gpu, case):
-    """PN_FLOW_SMMAP=1: table rows chosen by the SM each CTA runs on."""
-    aug, ref = case
-    with env(PN_MGS_MODE="flow", PN_FLOW_SMMAP="1"):
-        _check(_solve(aug), ref)
-
-
-def test_flow_table_file(gpu, case, tmp_path):
-    """A shuffled ownership table (296 CTAs, columns dealt at random)."""
-    aug, ref = case
-    rng = np.random.default_rng(5)
-    cols = rng.permutation(N + 1)
-    path = tmp_path / "own.txt"
-    path.write_text("\n".join(" ".join(str(j) for j in sorted(cols[c::296])) for c in range(296)) + "\n")
-    with env(PN_MGS_MODE="flow", PN_FLOW_OWN=str(path)):
-        _check(_solve(aug), ref)
-
-
-def test_flow_table_missing_column_refused(gpu, case, tmp_path):
-    aug, _ = case
-    path = tmp_path / "bad.txt"
-    path.write_text("\n".join(" ".join(str(j) for j in range(c, N, 296)) for c in range(296)) + "\n")  # no column N
-    with env(PN_MGS_MODE="flow", PN_FLOW_OWN=str(path)):
-        with pytest.raises(Exception, match="owned 0 times"):
-            _solve(aug)

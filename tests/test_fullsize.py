@@ -137,13 +137,3 @@ def test_cqd_tail_split_vs_oracle(gpu, m, n):
     assert same(res.factors.Q, Q)
     assert same(res.x, x)
     assert res.z == z
-
-
-@pytest.mark.parametrize("m,n", [(1536, 64), (700, 300)])
-def test_cqd_tail_cluster_vs_oracle(gpu, monkeypatch, m, n):
-    """PN_MGS_TAIL_CLUSTER=1: the row parts of a tail column form a
-    thread-block cluster and exchange partial sums through distributed shared
-    memory instead of global flags; the tree order and so Q, R, x, z are
-    unchanged."""
-    monkeypatch.setenv("PN_MGS_TAIL_CLUSTER", "1")
-    test_cqd_tail_split_vs_oracle(gpu, m, n)

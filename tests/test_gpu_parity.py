@@ -186,9 +186,9 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps", "warp", "pipe", "small"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "pipe", "small"])
 def mgs_mode(request, monkeypatch):
-    """Every MGS schedule (priority flow, dataflow, launch per sweep, warp per column)."""
+    """Every MGS schedule (priority flow, dataflow, launch per sweep, TMA pipe, one CTA)."""
     monkeypatch.setenv("PN_MGS_MODE", request.param)
     return request.param
 

@@ -245,3 +245,21 @@ def test_cyclic_packed_equals_object_builder():
                          (a.exps, b.exps), (a.coeffs, b.coeffs)):
                 assert np.array_equal(x, y)
             assert np.array_equal(np.signbit(a.coeffs), np.signbit(b.coeffs))
+
+
+def test_point_planes_refuses_wrong_shape_and_dtype():
+    """The C ABI reads exactly cshape * n doubles from the point pointer, so
+    the Python boundary refuses any other shape."""
+    import numpy as np
+    import pytest
+    from paper_1402_2626_b200.evaldiff import point_planes
+    from paper_1402_2626_b200.xprec import precision_level
+    cdd = precision_level("dd", True)
+    ok = point_planes(np.zeros((2, 2, 5)), cdd, 5)
+    assert ok.shape == (2, 2, 5) and ok.dtype == np.float64
+    assert point_planes(np.zeros((2, 2, 3, 5)), cdd, 5, 3).shape == (2, 2, 3, 5)
+    for bad in (np.zeros((2, 1, 5)), np.zeros((2, 2, 4)), np.zeros((2, 5)), np.zeros((2, 2, 2, 5))):
+        with pytest.raises(ValueError):
+            point_planes(bad, cdd, 5)
+    # float32 input is converted, not reinterpreted
+    assert point_planes(np.ones((2, 2, 5), np.float32), cdd, 5).dtype == np.float64
