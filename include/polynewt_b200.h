@@ -51,6 +51,7 @@ extern "C" {
 #define PN_E_DOMAIN 4    /* xprec.DomainError                              */
 #define PN_E_CUDA 5      /* CUDA runtime failure (RuntimeError)            */
 #define PN_E_NOMEM 6     /* device or host allocation failure              */
+#define PN_E_COMM 7      /* NCCL unavailable or failed (RuntimeError)      */
 
 /* element-wise op codes for pn_vec_op (VecContext methods) */
 #define PN_OP_ADD 0
@@ -208,6 +209,27 @@ int pn_evaldiff_batch(pn_system *sys, int64_t B, const double *x, double *f, voi
 int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t kmin, int32_t k, int32_t maxexp,
                               uint64_t seed, int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx, int32_t *exps,
                               double *coef_re, double *coef_im);
+
+/* ---- the batched path's collective (config C5 over several GPUs) ------------- */
+/* SURVEY 8(b) pn_comm_* / 8(e).  One process per GPU: rank 0 creates an id
+ * with pn_comm_unique_id and the host hands its 128 bytes to every rank (any
+ * out-of-band channel); each rank calls pn_comm_init.  pn_batch_allgather
+ * is the run's only collective: every rank contributes the results of its
+ * block of starts [lo, hi) = batch.shard_range(B, world, rank) -- x planes
+ * (cshape, hi - lo, n), iteration counts and status words as
+ * pn_newton_batch returns them -- and receives the full batch (x planes
+ * (cshape, B, n)).  Host or device pointers.  NCCL is loaded at run time
+ * (the process's own copy when it has one); PN_E_COMM if unavailable.
+ * Replaces batch.gather_batch's torch.distributed all_gather for hosts
+ * without PyTorch. */
+#define PN_COMM_ID_BYTES 128
+typedef struct pn_comm pn_comm;
+int pn_comm_unique_id(unsigned char *id);
+int pn_comm_init(int world, int rank, const unsigned char *id, int device, pn_comm **out);
+int pn_comm_destroy(pn_comm *comm);
+int pn_batch_allgather(pn_comm *comm, int nc, int cplx, int32_t n, int64_t B, const double *x_shard,
+                       const int32_t *iters_shard, const int32_t *status_shard, double *x_all, int32_t *iters_all,
+                       int32_t *status_all, void *stream);
 
 #ifdef __cplusplus
 }

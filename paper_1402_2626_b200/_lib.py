@@ -25,6 +25,7 @@ PN_E_SINGULAR = 3
 PN_E_DOMAIN = 4
 PN_E_CUDA = 5
 PN_E_NOMEM = 6
+PN_E_COMM = 7
 
 OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_ABS2, OP_SQRT, OP_CONJ, OP_MODULUS, OP_DIV_REAL = range(9)
 
@@ -71,6 +72,13 @@ SIGNATURES = {
                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "pn_system_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "pn_system_get_stats": ([ctypes.c_void_p, ctypes.POINTER(SystemStats)], ctypes.c_int),
+    "pn_comm_unique_id": ([ctypes.c_void_p], ctypes.c_int),
+    "pn_comm_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
+                     ctypes.c_int),
+    "pn_comm_destroy": ([ctypes.c_void_p], ctypes.c_int),
+    "pn_batch_allgather": ([ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int32, ctypes.c_int64,
+                            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                            ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "pn_system_plan_info": ([ctypes.c_void_p, ctypes.POINTER(PlanInfo)], ctypes.c_int),
     "pn_system_canonical_order": ([ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
     "pn_system_counts": ([ctypes.c_void_p, ctypes.POINTER(Counts)], ctypes.c_int),

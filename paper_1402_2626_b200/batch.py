@@ -188,13 +188,62 @@ def gather_batch(shard: BatchResult, B: int, group=None) -> BatchResult:
     return BatchResult(np.ascontiguousarray(x), out["iters"].astype(np.int32), out["status"].astype(np.int32))
 
 
+class NcclComm:
+    """The C ABI's communicator (pn_comm_*): NCCL straight from the library,
+    no torch.distributed.  ``uid`` is the 128-byte id of
+    NcclComm.unique_id() created on rank 0 and handed to every rank."""
+
+    def __init__(self, world: int, rank: int, uid: bytes, device: int = 0):
+        if len(uid) != 128:
+            raise ValueError("a communicator id is 128 bytes")
+        self.world, self.rank = world, rank
+        self._h = ctypes.c_void_p()
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        _lib.check(_lib.load().pn_comm_init(world, rank, ctypes.cast(buf, ctypes.c_void_p), device,
+                                            ctypes.byref(self._h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_ubyte * 128)()
+        _lib.check(_lib.load().pn_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        return bytes(buf)
+
+    def gather_batch(self, shard: BatchResult, B: int, level: PrecisionLevel) -> BatchResult:
+        """pn_batch_allgather: every rank's shard_range block -> the full batch."""
+        n = shard.x.shape[-1]
+        x = np.ascontiguousarray(shard.x, dtype=np.float64)
+        it = np.ascontiguousarray(shard.iters, dtype=np.int32)
+        stt = np.ascontiguousarray(shard.status, dtype=np.int32)
+        lo, hi = shard_range(B, self.world, self.rank)
+        if x.shape != level.cshape + (hi - lo, n) or it.shape != (hi - lo,) or stt.shape != (hi - lo,):
+            raise ValueError("shard does not match shard_range(B, world, rank)")
+        X = np.empty(level.cshape + (B, n))
+        I = np.empty(B, np.int32)
+        S = np.empty(B, np.int32)
+        _lib.check(_lib.load().pn_batch_allgather(self._h, level.ncomp, int(level.cplx), n, B, _lib.ptr(x),
+                                                   _lib.ptr(it), _lib.ptr(stt), _lib.ptr(X), _lib.ptr(I),
+                                                   _lib.ptr(S), None))
+        return BatchResult(X, I, S)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.load().pn_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _prepare_shard(packed: PackedSystem, Zs: np.ndarray, t):
     system, consts = homotopy_batch(packed, Zs, t)
     return PreparedSystem(system), consts
 
 
 def run_batched(packed: PackedSystem, Z: np.ndarray, t, max_iters: int = 10, tol: float | None = None,
-                group=None, prepare=None, solve=None):
+                group=None, prepare=None, solve=None, comm: NcclComm | None = None):
     """Config C5 on this rank: the B starts Z (planes cshape + (B, n)) are
     split by shard_range over the process group, the rank builds the
     homotopy constants of its shard (homotopy_start_system semantics,
@@ -204,16 +253,21 @@ def run_batched(packed: PackedSystem, Z: np.ndarray, t, max_iters: int = 10, tol
 
     ``prepare(packed, Zs, t) -> (prep, consts)`` and ``solve(prep, Zs,
     consts, max_iters=, tol=) -> BatchResult`` default to the GPU path; the
-    CPU tests substitute stubs to check the orchestration with gloo."""
+    CPU tests substitute stubs to check the orchestration with gloo.  With
+    ``comm`` (an NcclComm) the gather is the C ABI's pn_batch_allgather
+    instead of torch.distributed."""
     import torch.distributed as dist
     init = dist.is_available() and dist.is_initialized()
-    world = dist.get_world_size(group) if init else 1
-    rank = dist.get_rank(group) if init else 0
+    world = comm.world if comm else dist.get_world_size(group) if init else 1
+    rank = comm.rank if comm else dist.get_rank(group) if init else 0
     B = Z.shape[-2]
     lo, hi = shard_range(B, world, rank)
     Zs = np.ascontiguousarray(Z[..., lo:hi, :])
     prep, consts = (prepare or _prepare_shard)(packed, Zs, t)
     shard = (solve or run_newton_batch)(prep, Zs, consts, max_iters=max_iters, tol=tol)
-    full = gather_batch(shard, B, group) if init else shard
+    if comm is not None:
+        full = comm.gather_batch(shard, B, packed.level if packed is not None else prep.level)
+    else:
+        full = gather_batch(shard, B, group) if init else shard
     return shard, full, (lo, hi)
 

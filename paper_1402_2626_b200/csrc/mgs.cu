@@ -749,6 +749,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
   __shared__ int s_ok;
   const int ci = blockIdx.x / S, part = blockIdx.x % S;
   const int j = kstop + ci;
+  if (g_mgs_trace && blockIdx.x == 0 && threadIdx.x == 0) g_mgs_trace[n + 1] = globaltimer();  // tail start
   const int tid = threadIdx.x;
   const int row0 = part * RQ + tid * B;
   const int valid = m - row0 <= 0 ? 0 : (m - row0 >= B ? B : m - row0);
@@ -865,7 +866,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_mgs_tail(double *__restrict__ 
       for (int q = 0; q < B; ++q)
         if (q < valid) estore(qc + (long long)(row0 + q) * es, ediv_prepared(a[q], p));
       __syncthreads();
-      if (tid == 0) red_release_add(ready + j, 1);
+      if (tid == 0) {
+        red_release_add(ready + j, 1);
+        if (g_mgs_trace && part == 0) g_mgs_trace[j] = globaltimer();
+      }
     }
   }
 }
@@ -1149,7 +1153,7 @@ static void trace_end(int n, unsigned long long *buf, cudaStream_t st) {
   PN_CHECK_CUDA(cudaMemcpyToSymbol(g_mgs_trace, &null, sizeof(null)));
   cudaFree(buf);
   if (FILE *f = fopen(getenv("PN_MGS_TRACE"), "w")) {
-    for (int k = 0; k <= n; ++k) fprintf(f, "%d %llu\n", k, h[k]);
+    for (int k = 0; k <= n + 1; ++k) fprintf(f, "%d %llu\n", k, h[k]);
     fclose(f);
   }
 }

@@ -259,3 +259,24 @@ def test_serial_batch_matches_slots_and_leaves_system_unchanged(gpu, monkeypatch
     assert same(serial.x, slots.x)
     assert np.array_equal(serial.iters, slots.iters) and np.array_equal(serial.status, slots.status)
     assert same(evaluate_system(prep, z0).f, before)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lv,B", [("cdd", 7), ("rqd", 1), ("cd", 300)])
+def test_nccl_comm_batch_allgather_world1(gpu, lv, B):
+    """The C ABI's collective (pn_comm_init + pn_batch_allgather) on a
+    world of one: the gathered batch is the shard, host and device buffers."""
+    from paper_1402_2626_b200.batch import BatchResult, NcclComm
+    level = level_from_name(lv)
+    rng = np.random.default_rng(B)
+    n = 9
+    shard = BatchResult(rng.standard_normal(level.cshape + (B, n)), rng.integers(0, 9, B).astype(np.int32),
+                        rng.integers(0, 4, B).astype(np.int32))
+    comm = NcclComm(1, 0, NcclComm.unique_id())
+    full = comm.gather_batch(shard, B, level)
+    assert np.array_equal(full.x, shard.x)
+    assert np.array_equal(full.iters, shard.iters) and np.array_equal(full.status, shard.status)
+    with pytest.raises(ValueError):
+        comm.gather_batch(BatchResult(shard.x[..., :-1, :], shard.iters, shard.status), B, level)
+    comm.close()
+
