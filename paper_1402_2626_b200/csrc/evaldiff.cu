@@ -478,6 +478,100 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
 }
 
 // ---------------------------------------------------------------------------
+// K1, 32 < k: one WARP per monomial (cyclic n-roots, the paper's large
+// products).  Same tree and operand order as k_mono_large, but the levels
+// live in a warp-private slice of shared memory and the warp synchronises
+// with __syncwarp only, so monomials of different warps proceed
+// independently and no CTA-wide barrier idles 256 threads on the top levels
+// of one tree.  The complements overwrite the levels in place (both
+// children of a node are read before either is written), so a monomial
+// needs 2*base elements: bucket bases up to 1024 (d), 512 (dd), 256 (qd)
+// with several warps per SM; larger trees take k_mono_large.
+template <class E, int NW>
+__global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict__ list, long long count, int base,
+                                                       const int32_t *__restrict__ mon_ptr,
+                                                       const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
+                                                       const int32_t *__restrict__ dst, const double *__restrict__ coeff,
+                                                       const double *__restrict__ x, const double *__restrict__ table,
+                                                       const int32_t *__restrict__ toff, double *__restrict__ contrib,
+                                                       BView bv) {
+  constexpr int es = Traits<E>::es;
+  {
+    const long long b = bslot(bv);
+    x += b * bv.x;
+    table += b * bv.t;
+    contrib += b * bv.c;
+  }
+  extern __shared__ __align__(16) double wsmem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  E *lvl = reinterpret_cast<E *>(wsmem) + (size_t)w * 2 * base;  // levels, then complements in place
+  const long long nwarps = (long long)gridDim.x * NW;
+  for (long long g = blockIdx.x * (long long)NW + w; g < count; g += nwarps) {
+    const int c = list[g];
+    const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
+    const int ell = k - base;  // every monomial of the bucket has floor_pow2(k) == base
+    const int32_t *__restrict__ mv = var + lo;
+    auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
+    // level 0 (evaldiff.py:63-65): slot t = v[t] * v[base+t] for t < ell
+    for (int t = lane; t < base; t += 32) {
+      E v = leaf(t);
+      if (t < ell) v = emul(v, leaf(base + t));
+      lvl[t] = v;
+    }
+    __syncwarp();
+    // upward sweep (evaldiff.py:67-72): level j at offset 2*base - (2*base >> j)
+    int off = 0;
+    for (int size = base; size > 1; size >>= 1) {
+      const int h = size / 2;
+      for (int t = lane; t < h; t += 32) lvl[off + size + t] = emul(lvl[off + t], lvl[off + t + h]);
+      off += size;
+      __syncwarp();
+    }
+    const E root = lvl[off];
+    const E co = eload<E>(coeff + (long long)c * es);
+    const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
+    if (lane == 0) estore(contrib + (long long)c * es, emul(scale, root));
+    // downward sweep of complements (evaldiff.py:89-98), in place: the
+    // size-2 level's pair becomes [L1, L0], then each level's pair (t, t+h)
+    // is replaced by (cmp[t] * L[t+h], cmp[t] * L[t])
+    int o2 = off - 2;
+    if (lane == 0) {
+      const E a0 = lvl[o2], a1 = lvl[o2 + 1];
+      lvl[o2] = a1;
+      lvl[o2 + 1] = a0;
+    }
+    __syncwarp();
+    for (int h = 2; h < base; h <<= 1) {
+      const int oprev = o2 - 2 * h;  // level of size 2h
+      for (int t = lane; t < h; t += 32) {
+        const E ct = lvl[o2 + t];
+        const E a = lvl[oprev + t], b2 = lvl[oprev + t + h];
+        lvl[oprev + t] = emul(ct, b2);
+        lvl[oprev + t + h] = emul(ct, a);
+      }
+      o2 = oprev;
+      __syncwarp();
+    }
+    // unfold folded pairs and scale (evaldiff.py:100-108, 174-180)
+    for (int t = lane; t < base; t += 32) {
+      const E cm = lvl[t];
+      if (t < ell) {
+        const int t2 = base + t;
+        const E g1 = emul(cm, leaf(t2));
+        const E g2 = emul(cm, leaf(t));
+        const int d1 = exps[lo + t], d2 = exps[lo + t2];
+        estore(contrib + (long long)dst[lo + t] * es, emul(d1 == 1 ? scale : emul_int(scale, d1), g1));
+        estore(contrib + (long long)dst[lo + t2] * es, emul(d2 == 1 ? scale : emul_int(scale, d2), g2));
+      } else {
+        const int d1 = exps[lo + t];
+        estore(contrib + (long long)dst[lo + t] * es, emul(d1 == 1 ? scale : emul_int(scale, d1), cm));
+      }
+    }
+    __syncwarp();  // the levels are rewritten by the warp's next monomial
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: one thread per output entry
 
 template <class E>
@@ -929,8 +1023,31 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
         default: PN_REQUIRE(false, PN_E_ARG, "internal: bad bucket base %d", b.base);
       }
     } else {
-      int base = 1;
-      while (base * 2 <= sys->max_k) base *= 2;
+      const int base = b.base;
+      // warp per monomial while a warp's levels (2*base elements) leave room
+      // for six warps per SM (PN_LARGE_WARP=0: CTA per monomial)
+      const char *wv = getenv("PN_LARGE_WARP");
+      const size_t wbytes = (size_t)2 * base * es * sizeof(double);
+      if (!(wv && strcmp(wv, "0") == 0) && wbytes * 6 <= 224 * 1024) {
+        auto launch = [&](auto kern, int NW) {
+          const size_t smem = NW * wbytes;
+          if (smem > 48 * 1024)
+            PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          int per_sm = 0;
+          PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
+          const long long blocks = (b.count + NW - 1) / NW;
+          const int gx =
+              (int)std::min<long long>(blocks, std::max(1LL, (long long)std::max(per_sm, 1) * num_sms() / nb));
+          kern<<<dim3(gx, nb), NW * 32, smem, st>>>(b.d_list, b.count, base, sys->d_mon_ptr, sys->d_var,
+                                                    sys->d_exp, sys->d_dst, sys->d_coeff, x, table, sys->d_toff,
+                                                    contrib, bv);
+        };
+        if (wbytes * 8 <= 224 * 1024) launch(k_mono_warp<E, 4>, 4);  // 4 warps per CTA
+        else launch(k_mono_warp<E, 2>, 2);                            // 2 per CTA, 3 CTAs per SM
+        PN_CHECK_LAUNCH();
+        count_launch(1);
+        continue;
+      }
       size_t smem = (size_t)3 * base * es * sizeof(double);
       constexpr int NT = 256;
       const int gx = (int)std::min<long long>(b.count, std::max(1LL, (long long)num_sms() * 8 / nb));

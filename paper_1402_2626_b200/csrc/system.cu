@@ -286,7 +286,8 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
   S.nseg = (long long)seg_out.size();
 
   // 5. buckets + analytic OpCounter + work counts
-  std::vector<std::vector<int32_t>> lists(8);  // 0: k<=1; 1..5: base 2..32; 6: large
+  // 0: k <= 1; 1..5: base 2..32; 6 + j: large trees of base 2^(6 + j)
+  std::vector<std::vector<int32_t>> lists(6 + 26);
   int64_t em = 0, gm = 0, mul_ops = 0, int_ops = 0;
   int max_k = 0;
   for (int64_t c = 0; c < M; ++c) {
@@ -312,18 +313,17 @@ extern "C" int pn_system_create(int nc, int cplx, int32_t m, int32_t n, int64_t 
     gm += (2 * base - 4) + 2 * ell + k + cc;         // gradient circuit + derivative scaling
     mul_ops += (k - 1) + cc + 1 + (2 * base - 4) + 2 * ell + k;
     int_ops += cc;
-    int lst = 6;
-    if (base <= 32) lst = __builtin_ctz(base);  // base 2 -> 1, ..., 32 -> 5
+    const int lst = __builtin_ctz(base);  // base 2 -> 1, ..., 32 -> 5, 64 -> 6, ...
     lists[lst].push_back((int32_t)c);
   }
   S.counts.eval_mults = em;
   S.counts.grad_mults = gm;
   S.max_k = max_k;
-  for (int b = 0; b < 7; ++b) {
+  for (int b = 0; b < (int)lists.size(); ++b) {
     if (lists[b].empty()) continue;
     pn_system::Bucket bk;
-    bk.kind = b == 0 ? 0 : (b == 6 ? 2 : 1);
-    bk.base = b >= 1 && b <= 5 ? (1 << b) : 0;
+    bk.kind = b == 0 ? 0 : (b >= 6 ? 2 : 1);
+    bk.base = b >= 1 ? (1 << b) : 0;
     bk.count = (long long)lists[b].size();
     bk.d_list = upload(lists[b]);
     if (bk.kind == 1) {

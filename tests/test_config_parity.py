@@ -222,3 +222,30 @@ def test_cyclic_1024_rows_vs_oracle(gpu, lv):
     f, J, _ = oracle.evaluate(oracle_level(lv), oracle.CSR.from_packed(p), x, nthreads=NT)
     assert same(ev.f, f)
     assert same(ev.J, J)
+
+
+@pytest.mark.parametrize("warp", ["1", "0"])
+@pytest.mark.parametrize("lv", ["cd", "cdd", "cqd", "rqd"])
+def test_cyclic_300_all_large_buckets_vs_oracle(gpu, monkeypatch, lv, warp):
+    """Full cyclic 300-roots (k = 1 .. 300: tree buckets up to base 32 and
+    the large buckets of base 64, 128, 256), evaluated with one warp per
+    large monomial (default) and one CTA per monomial (PN_LARGE_WARP=0);
+    sampled rows against the oracle."""
+    from paper_1402_2626_b200.evaldiff import PreparedSystem, evaluate_system
+    from paper_1402_2626_b200.generators import cyclic_packed
+    monkeypatch.setenv("PN_LARGE_WARP", warp)
+    n = 300
+    level = level_from_name(lv)
+    p = cyclic_packed(n, level)
+    rng = np.random.default_rng(17)
+    x = np.zeros(level.cshape + (n,))
+    if level.cplx:
+        theta = rng.uniform(0.0, 2.0 * np.pi, n)
+        x[0, 0], x[1, 0] = np.cos(theta), np.sin(theta)
+    else:
+        x[0] = rng.uniform(0.9, 1.1, n) * rng.choice([-1.0, 1.0], n)
+    ev = evaluate_system(PreparedSystem(p), x)
+    rows = [0, 31, 32, 63, 64, 100, 127, 128, 255, 256, 298, 299]
+    f, J, _ = oracle.evaluate(oracle_level(lv), oracle.CSR.from_packed(p).rows(rows), x, nthreads=NT)
+    assert same(ev.f[..., rows], f)
+    assert same(ev.J[..., rows, :], J)
