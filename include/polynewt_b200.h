@@ -210,6 +210,20 @@ int pn_generate_random_system(int32_t m, int32_t n, int32_t T, int32_t kmin, int
                               uint64_t seed, int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx, int32_t *exps,
                               double *coef_re, double *coef_im);
 
+/* ---- system text format (polyrep.py:140-304) ------------------------------- */
+/* Native ingestion of the text format into CSR (generation order) and
+ * coefficient planes (es, M), the components converted exactly as
+ * parse_decimal (xprec.py:432-446).  PN_E_ARG for malformed input and for
+ * constructs outside the native scanner (non-ASCII text, unusual numeric
+ * forms): the host then re-parses with polyrep.parse_system, which raises
+ * the reference's SystemParseError or builds the system. */
+typedef struct pn_text_system pn_text_system;
+int pn_parse_system(const char *text, int64_t len, int nc, int cplx, pn_text_system **out);
+int pn_text_system_sizes(const pn_text_system *s, int32_t *m, int32_t *n, int64_t *M, int64_t *nnz);
+int pn_text_system_export(const pn_text_system *s, int32_t *poly_ptr, int32_t *mon_ptr, int32_t *var_idx,
+                          int32_t *exps, double *coeff_planes);
+int pn_text_system_free(pn_text_system *s);
+
 /* ---- the batched path's collective (config C5 over several GPUs) ------------- */
 /* SURVEY 8(b) pn_comm_* / 8(e).  One process per GPU: rank 0 creates an id
  * with pn_comm_unique_id and the host hands its 128 bytes to every rank (any

@@ -72,6 +72,13 @@ SIGNATURES = {
                           ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "pn_system_destroy": ([ctypes.c_void_p], ctypes.c_int),
     "pn_system_get_stats": ([ctypes.c_void_p, ctypes.POINTER(SystemStats)], ctypes.c_int),
+    "pn_parse_system": ([ctypes.c_char_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
+                        ctypes.c_int),
+    "pn_text_system_sizes": ([ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "pn_text_system_export": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p], ctypes.c_int),
+    "pn_text_system_free": ([ctypes.c_void_p], ctypes.c_int),
     "pn_comm_unique_id": ([ctypes.c_void_p], ctypes.c_int),
     "pn_comm_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)],
                      ctypes.c_int),

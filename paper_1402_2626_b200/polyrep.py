@@ -347,3 +347,36 @@ def _read_term(cur: _Text, level: PrecisionLevel, n_vars: int, negate: bool):
         return Monomial(coeff, tuple(sorted(powers.items())))
     except ValueError as exc:
         cur.fail(str(exc))
+
+
+def parse_system_packed(text: str, level: PrecisionLevel) -> PackedSystem:
+    """The text format straight into a PackedSystem (generation order) by
+    the native scanner (pn_parse_system: CSR and exact coefficient
+    components without Monomial objects -- for 10^6-monomial files).  Input
+    the native scanner refuses (malformed text, or forms only Python's
+    Decimal / str methods accept) goes through parse_system, so errors are
+    the reference's SystemParseError with its line and column."""
+    import ctypes
+
+    from . import _lib
+    raw = text.encode("utf-8")
+    h = ctypes.c_void_p()
+    lib = _lib.load()
+    rc = lib.pn_parse_system(raw, len(raw), level.ncomp, int(level.cplx), ctypes.byref(h))
+    if rc != 0:
+        return PackedSystem.from_system(parse_system(text, level), level)
+    try:
+        m, n = ctypes.c_int32(), ctypes.c_int32()
+        M, nnz = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(lib.pn_text_system_sizes(h, ctypes.byref(m), ctypes.byref(n), ctypes.byref(M), ctypes.byref(nnz)))
+        poly_ptr = np.empty(m.value + 1, np.int32)
+        mon_ptr = np.empty(M.value + 1, np.int32)
+        var_idx = np.empty(nnz.value, np.int32)
+        exps = np.empty(nnz.value, np.int32)
+        coeffs = np.empty(level.cshape + (M.value,))
+        _lib.check(lib.pn_text_system_export(h, _lib.ptr(poly_ptr), _lib.ptr(mon_ptr), _lib.ptr(var_idx),
+                                             _lib.ptr(exps), _lib.ptr(coeffs)))
+    finally:
+        lib.pn_text_system_free(h)
+    return PackedSystem(level, n.value, poly_ptr, mon_ptr, var_idx, exps, coeffs)
+

@@ -13,6 +13,8 @@ CAPTURES = [  # (raw csv, kernel, workload, details csv named in "source")
     ("bsub", "k_backsub_look", "F(1024,1024,32) complex qd 1024x1024"),
     ("tail", "k_mgs_tail", "F(1024,1024,32) complex qd 1024x1024"),
     ("pipe", "k_mgs_pipe", "F(1024,1024,32) complex dd 1024x1024"),
+    ("piped", "k_mgs_pipe", "F(1024,1024,32) complex d 1024x1024"),
+    ("rows", "k_eval_rows", "F(1024,1024,32) complex d 1024x1024"),
     ("solve", "k_solve_batch", "C5 296 slots F(256,256,32) complex dd"),
 ]
 
