@@ -94,3 +94,17 @@ def test_qr_check_and_evaldiff(gpu):
     # the product tree's analytic counts (test_acceptance.py:46-61): n-1 and 2n-4 per product
     assert d["tree"]["eval_mults"] == 4 * 63 and d["tree"]["grad_mults"] == 4 * 124
     assert d["sequential"]["eval_mults"] == 4 * 63 and d["sequential"]["grad_mults"] == 4 * 124
+
+
+@pytest.mark.gpu
+def test_newton_from_text_file_matches_benchmark(gpu, tmp_path):
+    """gen -> file -> newton --file (native text ingestion) gives the same
+    trace as newton --benchmark on the same system."""
+    g = _golden()
+    path = tmp_path / "chandra12.txt"
+    r = _cli("gen", "--benchmark", "chandrasekhar", "--n", "12", "--output", str(path))
+    assert r.returncode == 0, r.stderr
+    out = tmp_path / "t.jsonl"
+    r = _cli("newton", "--file", str(path), "--iters", "6", "--tol", "0", "--output", str(out))
+    assert r.returncode == 0, r.stderr
+    assert "".join(out.read_text().splitlines(keepends=True)[:-1]) == g["newton_chandrasekhar_12_cdd"]
