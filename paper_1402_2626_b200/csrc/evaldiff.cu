@@ -529,7 +529,11 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
     }
     const E root = lvl[off];
     const E co = eload<E>(coeff + (long long)c * es);
-    const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
+    // the common factor (polyrep.py:133-139) only when an exponent is >= 2:
+    // one coalesced pass of the warp over the exponents decides it
+    bool multi = false;
+    for (int t = lane; t < k; t += 32) multi |= exps[lo + t] >= 2;
+    const E scale = __any_sync(0xffffffffu, multi) ? monomial_scale<E>(co, lo, k, var, exps, table, toff) : co;
     if (lane == 0) estore(contrib + (long long)c * es, emul(scale, root));
     // downward sweep of complements (evaldiff.py:89-98), in place: the
     // size-2 level's pair becomes [L1, L0], then each level's pair (t, t+h)
