@@ -432,9 +432,13 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
       __syncthreads();
     }
     const E root = lvl[off];
+    // common factor only when some exponent is >= 2 (one parallel pass)
+    bool multi_t = false;
+    for (int t = threadIdx.x; t < k; t += NT) multi_t |= exps[lo + t] >= 2;
+    const bool multi = __syncthreads_or(multi_t);
     if (threadIdx.x == 0) {
       const E co = eload<E>(coeff + (long long)c * es);
-      const E scale = monomial_scale<E>(co, lo, k, var, exps, table, toff);
+      const E scale = multi ? monomial_scale<E>(co, lo, k, var, exps, table, toff) : co;
       s_scale = scale;
       estore(contrib + (long long)c * es, emul(scale, root));
     }
