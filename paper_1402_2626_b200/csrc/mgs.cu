@@ -1440,6 +1440,16 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
+  // d/dd columns of 2048 < m <= 4096 rows: the flow kernel with 1024-thread
+  // CTAs (4 rows per thread, the working column in shared memory, one CTA
+  // per SM) instead of the streaming dataflow kernel -- Chandrasekhar
+  // n = 4096 cdd, 6 Newton steps 9.9 -> 6.2 s (equal at 2048).
+  // PN_FLOW_WIDE=0|1 forces it off / on for 1024 < m <= 4096.
+  if (mode == 4 && Traits<E>::nc <= 2 && m > 1024 && m <= 4096) {
+    const char *fw = getenv("PN_FLOW_WIDE");
+    const bool wide = fw ? strcmp(fw, "1") == 0 : m > 2048;
+    if (wide && flow_launch<E, 4, 1024>(m, n, A, Q, R, w, st)) return;
+  }
   if (mode <= 1 || mode == 4) {
     int per_sm = 0;
     PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mgs_dataflow<E, B>, kMgsThreads, 0));

@@ -249,3 +249,21 @@ def test_cyclic_300_all_large_buckets_vs_oracle(gpu, monkeypatch, lv, warp):
     f, J, _ = oracle.evaluate(oracle_level(lv), oracle.CSR.from_packed(p).rows(rows), x, nthreads=NT)
     assert same(ev.f[..., rows], f)
     assert same(ev.J[..., rows, :], J)
+
+
+@pytest.mark.parametrize("lv,m,n", [("cdd", 4096, 48), ("cd", 3000, 200), ("rdd", 2100, 130)])
+@pytest.mark.parametrize("wide", ["1", "0"])
+def test_tall_least_squares_wide_flow_vs_oracle(gpu, monkeypatch, lv, m, n, wide):
+    """d/dd with 1024 < m <= 4096 rows: the 1024-thread flow kernel (default
+    above 2048 rows, PN_FLOW_WIDE) and the dataflow kernel, against the
+    oracle (the shapes of the Chandrasekhar n = 2048..4096 runs)."""
+    from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
+    from paper_1402_2626_b200.varith import VecContext
+    monkeypatch.setenv("PN_FLOW_WIDE", wide)
+    L, aug = _busy_aug(lv, m, n, m + n)
+    res = least_squares_solve(AugmentedMatrix(VecContext(level_from_name(lv)), aug))
+    x, z, Q, R = oracle.least_squares(L, aug, nthreads=NT)
+    assert same(res.factors.R, R)
+    assert same(res.factors.Q, Q)
+    assert same(res.x, x)
+    assert res.z == z
