@@ -488,10 +488,12 @@ __global__ void __launch_bounds__(NT) k_mono_large(const int32_t *__restrict__ l
 // with __syncwarp only, so monomials of different warps proceed
 // independently and no CTA-wide barrier idles 256 threads on the top levels
 // of one tree.  The complements overwrite the levels in place (both
-// children of a node are read before either is written), so a monomial
-// needs 2*base elements: bucket bases up to 1024 (d), 512 (dd), 256 (qd)
-// with several warps per SM; larger trees take k_mono_large.
-template <class E, int NW>
+// children of a node are read before either is written); for dd/qd level 0
+// is recomputed from x instead of stored, so a monomial needs base - 1
+// elements (qd base 256: 16 KB, twelve warps per SM; cyclic 448-roots qd
+// 23.6 -> 20.6 ms), for d 2 * base; trees too wide for six warps per SM
+// take k_mono_large.
+template <class E, int NW, bool LEAN>
 __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict__ list, long long count, int base,
                                                        const int32_t *__restrict__ mon_ptr,
                                                        const int32_t *__restrict__ var, const int32_t *__restrict__ exps,
@@ -508,24 +510,35 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
   }
   extern __shared__ __align__(16) double wsmem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  E *lvl = reinterpret_cast<E *>(wsmem) + (size_t)w * 2 * base;  // levels, then complements in place
+  // LEAN (dd, qd): levels 1.. only (base - 1 elements; level 0 -- the slots --
+  // is recomputed from x when the complements reach it); otherwise (d,
+  // where the extra loads cost more than the storage saves) levels 0.. in
+  // 2 * base elements.  The complements then overwrite the levels in place.
+  E *lvl = reinterpret_cast<E *>(wsmem) + (size_t)w * (LEAN ? base : 2 * base);
   const long long nwarps = (long long)gridDim.x * NW;
+  const int h0 = base / 2;  // size of level 1 (base >= 64 here)
   for (long long g = blockIdx.x * (long long)NW + w; g < count; g += nwarps) {
     const int c = list[g];
     const int lo = mon_ptr[c], k = mon_ptr[c + 1] - lo;
     const int ell = k - base;  // every monomial of the bucket has floor_pow2(k) == base
     const int32_t *__restrict__ mv = var + lo;
     auto leaf = [&](int t) -> E { return eload_ldg<E>(x + (long long)mv[t] * es); };
-    // level 0 (evaldiff.py:63-65): slot t = v[t] * v[base+t] for t < ell
-    for (int t = lane; t < base; t += 32) {
+    // slot t of level 0 (evaldiff.py:63-65): v[t] * v[base+t] for t < ell
+    auto slot = [&](int t) -> E {
       E v = leaf(t);
       if (t < ell) v = emul(v, leaf(base + t));
-      lvl[t] = v;
+      return v;
+    };
+    // upward sweep (evaldiff.py:67-72): each level stored right after the
+    // previous one, starting with level 1 (LEAN) or level 0
+    int off = 0;
+    if constexpr (LEAN) {
+      for (int t = lane; t < h0; t += 32) lvl[t] = emul(slot(t), slot(t + h0));
+    } else {
+      for (int t = lane; t < base; t += 32) lvl[t] = slot(t);
     }
     __syncwarp();
-    // upward sweep (evaldiff.py:67-72): level j at offset 2*base - (2*base >> j)
-    int off = 0;
-    for (int size = base; size > 1; size >>= 1) {
+    for (int size = LEAN ? h0 : base; size > 1; size >>= 1) {
       const int h = size / 2;
       for (int t = lane; t < h; t += 32) lvl[off + size + t] = emul(lvl[off + t], lvl[off + t + h]);
       off += size;
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
     if (lane == 0) estore(contrib + (long long)c * es, emul(scale, root));
     // downward sweep of complements (evaldiff.py:89-98), in place: the
     // size-2 level's pair becomes [L1, L0], then each level's pair (t, t+h)
-    // is replaced by (cmp[t] * L[t+h], cmp[t] * L[t])
+    // is replaced by (cmp[t] * L[t+h], cmp[t] * L[t]) down to level 1
     int o2 = off - 2;
     if (lane == 0) {
       const E a0 = lvl[o2], a1 = lvl[o2 + 1];
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
       lvl[o2 + 1] = a0;
     }
     __syncwarp();
-    for (int h = 2; h < base; h <<= 1) {
+    for (int h = 2; h < (LEAN ? h0 : base); h <<= 1) {
       const int oprev = o2 - 2 * h;  // level of size 2h
       for (int t = lane; t < h; t += 32) {
         const E ct = lvl[o2 + t];
@@ -560,9 +573,9 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
       o2 = oprev;
       __syncwarp();
     }
+    // level 0's complements from level 1's and the recomputed slots, then
     // unfold folded pairs and scale (evaldiff.py:100-108, 174-180)
-    for (int t = lane; t < base; t += 32) {
-      const E cm = lvl[t];
+    auto emit = [&](int t, const E &cm) {
       if (t < ell) {
         const int t2 = base + t;
         const E g1 = emul(cm, leaf(t2));
@@ -574,6 +587,16 @@ __global__ void __launch_bounds__(NW * 32) k_mono_warp(const int32_t *__restrict
         const int d1 = exps[lo + t];
         estore(contrib + (long long)dst[lo + t] * es, emul(d1 == 1 ? scale : emul_int(scale, d1), cm));
       }
+    };
+    if constexpr (LEAN) {
+      for (int t = lane; t < h0; t += 32) {
+        const E c1 = lvl[t];
+        const E s0 = slot(t), s1 = slot(t + h0);
+        emit(t, emul(c1, s1));
+        emit(t + h0, emul(c1, s0));
+      }
+    } else {
+      for (int t = lane; t < base; t += 32) emit(t, lvl[t]);
     }
     __syncwarp();  // the levels are rewritten by the warp's next monomial
   }
@@ -1035,7 +1058,8 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
       // warp per monomial while a warp's levels (2*base elements) leave room
       // for six warps per SM (PN_LARGE_WARP=0: CTA per monomial)
       const char *wv = getenv("PN_LARGE_WARP");
-      const size_t wbytes = (size_t)2 * base * es * sizeof(double);
+      constexpr bool lean = Traits<E>::nc >= 2;
+      const size_t wbytes = (size_t)(lean ? base : 2 * base) * es * sizeof(double);
       if (!(wv && strcmp(wv, "0") == 0) && wbytes * 6 <= 224 * 1024) {
         auto launch = [&](auto kern, int NW) {
           const size_t smem = NW * wbytes;
@@ -1050,8 +1074,8 @@ static void evaldiff_run(pn_system *sys, const double *x, double *table, double 
                                                     sys->d_exp, sys->d_dst, sys->d_coeff, x, table, sys->d_toff,
                                                     contrib, bv);
         };
-        if (wbytes * 8 <= 224 * 1024) launch(k_mono_warp<E, 4>, 4);  // 4 warps per CTA
-        else launch(k_mono_warp<E, 2>, 2);                            // 2 per CTA, 3 CTAs per SM
+        if (wbytes * 8 <= 224 * 1024) launch(k_mono_warp<E, 4, lean>, 4);  // 4 warps per CTA
+        else launch(k_mono_warp<E, 2, lean>, 2);                            // 2 per CTA, 3 CTAs per SM
         PN_CHECK_LAUNCH();
         count_launch(1);
         continue;
