@@ -481,7 +481,8 @@ template <class E, int B, int NT>
 __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_flow(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                     double eps, double *__restrict__ Q, double *__restrict__ R,
                                                     MgsStatus *status, int *ready, int kstop, int hold, int lag,
-                                                    const int *__restrict__ own, int maxo, int pickrule) {
+                                                    const int *__restrict__ own, int maxo, int pickrule,
+                                                    bool qcache) {
   using Rl = typename Traits<E>::R;
   constexpr int es = Traits<E>::es;
   constexpr int D = Depth<B>::value;
@@ -589,6 +590,11 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
     }
     poll();
   };
+  // q rows: through L1 when qcache (the second read of a row and the other
+  // half of each 32-byte sector hit L1), else L2 only.  Safe: a q column is
+  // written once per launch before its release flag, nobody reads it earlier,
+  // and its lines are whole (the column is a multiple of 128 bytes).
+  auto qload = [&](const double *p) -> E { return qcache ? eload<E>(p) : eload_cg<E>(p); };
   // one sweep k applied to the resident column j (mgs.py:201-215)
   auto apply = [&](int k, int j) {
     const double *qk = Q + (long long)k * m * es;
@@ -596,13 +602,13 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : NT <= 256 ? 2 : 1) k_mgs_f
 #pragma unroll
     for (int q = 0; q < B; ++q) {
       const int r = row0 + q;
-      if (r < m) pw.push(emul(econj(eload_cg<E>(qk + (long long)r * es)), col.get(r)));
+      if (r < m) pw.push(emul(econj(qload(qk + (long long)r * es)), col.get(r)));
     }
     const E rk = reduce2(pw.fold(), &s_pe[0][0], s_re);
 #pragma unroll
     for (int q = 0; q < B; ++q) {
       const int r = row0 + q;
-      if (r < m) col.put(r, esub(col.get(r), emul(eload_cg<E>(qk + (long long)r * es), rk)));
+      if (r < m) col.put(r, esub(col.get(r), emul(qload(qk + (long long)r * es), rk)));
     }
     if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, rk);
   };
@@ -1263,7 +1269,12 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   // cqd MGS 107.5 -> 106.8 ms), 0 = lowest index (earliest deadline)
   const char *pv = getenv("PN_FLOW_PICK");
   int pickrule = pv ? atoi(pv) : 1;
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule};
+  // q rows through L1 (cqd factorisation 103.25 -> 102.72 ms, profiles/r02/exp
+  // ab7); PN_FLOW_QCACHE=0 streams them from L2 only
+  const char *qc = getenv("PN_FLOW_QCACHE");
+  bool qcache = !(qc && strcmp(qc, "0") == 0) && ((long long)m * Traits<E>::es * 8) % 128 == 0;
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &kstop, &hold, &lag, &own, &maxo, &pickrule,
+                  &qcache};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
