@@ -225,9 +225,15 @@ __device__ __forceinline__ void rs_level(E (&v)[P], int t, int nparts) {
 // the CTA-uniform parity `par` (flipped here), so consecutive reductions
 // need no trailing barrier.  The tree over the warps' partials runs on warp
 // 0 with 32/P lanes per column (a local pairwise tree over each lane's warp
-// partials, then shuffle levels), not serially in one thread.
-template <class E, int P, int NT>
-__device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout, int &par) {
+// partials, then shuffle levels), not serially in one thread.  `mid` runs on
+// every thread right after the first barrier (every thread has finished all
+// earlier work of the CTA there).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <class E, int P, int NT, class Hook = NoHook>
+__device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout, int &par,
+                                                  const Hook &mid = Hook()) {
   constexpr int NW = NT / 32;
   constexpr int LPC0 = 32 / P;
   constexpr int LPC = LPC0 < NW ? LPC0 : NW;  // lanes per column
@@ -238,6 +244,7 @@ __device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred
   rs_level<E, P, 0>(v, t, nparts);
   if (lane < P) sr[w * P + rs_col<P>(lane)] = v[0];
   __syncthreads();
+  mid();
   if (w == 0) {
     const int nw = (nparts + 31) / 32;
     const int c = lane / LPC, jl = lane % LPC;

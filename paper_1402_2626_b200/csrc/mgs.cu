@@ -901,10 +901,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // block sums of NQ aligned 256-row blocks (reduce-scatter), then their
 // pairwise tree (absorb rule over the blocks)
-template <class T, int P, int NQ, int NT>
-__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par) {
+template <class T, int P, int NQ, int NT, class Hook = NoHook>
+__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par, const Hook &mid = Hook()) {
   const T *res = out + par * P;
-  multi_tree_reduce<T, P, NT>(v, NT, part, out, par);
+  multi_tree_reduce<T, P, NT>(v, NT, part, out, par, mid);
   T acc = res[0];
   if constexpr (NQ == 2) acc = eadd(res[0], res[1]);
   if constexpr (NQ == 3) acc = eadd(eadd(res[0], res[1]), res[2]);
@@ -915,7 +915,7 @@ __device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par
 template <class E, int NQ, int QB>
 __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                      double eps, double *__restrict__ Q, double *__restrict__ R,
-                                                     MgsStatus *status, int *ready) {
+                                                     MgsStatus *status, int *ready, int late) {
   using Rl = typename Traits<E>::R;
   constexpr int NT = 256;
   constexpr int es = Traits<E>::es;
@@ -1002,10 +1002,37 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     bulk_g2s(qbuf + (size_t)b * m, Q + (long long)k * m * es, cbytes, &bar[2 + b]);
   };
   if (tid == 0 && first_after(0) <= n) issue_col(first_after(0), 0);
+  // pivot wait with one barrier: s_ok is rewritten only at the next sweep's
+  // wait, and every sweep has at least one apply (two reduction barriers) in
+  // between
+  __shared__ int s_ok;
+  auto wait1 = [&](int k) -> bool {
+    if (tid == 0) {
+      long long t0 = clock64();
+      int ok = 1;
+      while (ld_acquire(ready + k) == 0) {
+        __nanosleep(64);
+        if (ld_acquire(&status->code) != 0) {
+          ok = 0;
+          break;
+        }
+        if (clock64() - t0 > (1ll << 36)) {
+          status->k = k;
+          atomicExch(&status->code, PN_E_CUDA);
+          ok = 0;
+          break;
+        }
+      }
+      if (ok && ld_acquire(&status->code) != 0) ok = 0;
+      s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+  };
   for (int k = 0; k < n; ++k) {
     const int j0 = first_after(k);
     if (j0 > n) break;
-    if (!wait_pivot(ready, k, status)) return;
+    if ((late & 2) ? !wait_pivot(ready, k, status) : !wait1(k)) return;
     if (QB == 2) qs = k & 1;
     if (tid == 0 && qpre != k) issue_q(k, qs);
     mbar_wait(&bar[2 + qs], ph[2 + qs]);
@@ -1015,7 +1042,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       int jn = j + G;
       if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
       const bool pf = jn <= n && jn != j;
-      if (pf && tid == 0) issue_col(jn, s ^ 1);
+      // late: the prefetch goes out after the first barrier of this apply's
+      // reduction (everyone is done with the other buffer there), so no
+      // barrier closes the apply
+      if (!(late & 1) && pf && tid == 0) issue_col(jn, s ^ 1);
       // q_{k+1} into the other buffer as soon as it is published (its last
       // reader, sweep k-1, finished before this sweep's first barrier)
       if (QB == 2 && tid == 0 && qpre != k + 1 && k + 1 < n && first_after(k + 1) <= n &&
@@ -1039,7 +1069,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
           v[q] = ezero<E>();
         }
       }
-      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par);
+      const auto mid = [&]() {
+        if ((late & 1) && pf && tid == 0) issue_col(jn, s ^ 1);
+      };
+      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par, mid);
       double *col = A + (long long)j * m * es;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -1050,7 +1083,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       fence_proxy_async();
       if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
       if (j == k + 1 && !pivot(k + 1, a)) return;
-      __syncthreads();  // colb[s] and the reduction slots are free
+      if (!(late & 1)) __syncthreads();  // colb[s] and the reduction slots are free
       if (pf) {
         s ^= 1;
         inbuf = -1;
@@ -1311,7 +1344,13 @@ static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   w.ready.ensure((size_t)(n + 1) * sizeof(int));
   PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
   int *ready = w.ready.as<int>();
-  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready};
+  // PN_PIPE_LATE bit 0: late prefetch (no closing barrier per apply): cdd
+  // factorisation 16.13 -> 15.99 ms; cd 5.05 -> 7.46 ms (its short applies no
+  // longer cover the column copy), so double double only (profiles/r02/exp
+  // ab8/ab9).  Bit 1: the two-barrier pivot wait instead of the one-barrier one.
+  const char *lv = getenv("PN_PIPE_LATE");
+  int late = lv ? atoi(lv) : (Traits<E>::nc == 2 ? 1 : 0);
+  void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &late};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
   PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, 256, args, smem, st));

@@ -186,11 +186,15 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps", "pipe", "small"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "pipe/late0", "pipe/late1", "small"])
 def mgs_mode(request, monkeypatch):
-    """Every MGS schedule (priority flow, dataflow, launch per sweep, TMA pipe, one CTA)."""
-    monkeypatch.setenv("PN_MGS_MODE", request.param)
-    return request.param
+    """Every MGS schedule (priority flow, dataflow, launch per sweep, TMA pipe
+    with the prefetch before the reduction or after its first barrier, one CTA)."""
+    mode, _, late = request.param.partition("/late")
+    monkeypatch.setenv("PN_MGS_MODE", mode)
+    if late:
+        monkeypatch.setenv("PN_PIPE_LATE", late)
+    return mode
 
 
 @pytest.mark.parametrize("name", [n for n in golden_names("mgs_") if "breakdown" not in n])
