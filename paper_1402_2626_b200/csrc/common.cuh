@@ -231,7 +231,11 @@ __device__ __forceinline__ void rs_level(E (&v)[P], int t, int nparts) {
 struct NoHook {
   __device__ __forceinline__ void operator()() const {}
 };
-template <class E, int P, int NT, class Hook = NoHook>
+// FOLD > 0: the P column results are the sums of FOLD consecutive aligned
+// row blocks of one column; warp 0 also folds them by their pairwise tree
+// (two shuffle levels for P = 4) and sout[par * P] gets the one total, so
+// the other warps read one value instead of each repeating the fold.
+template <class E, int P, int NT, int FOLD = 0, class Hook = NoHook>
 __device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred, E *sout, int &par,
                                                   const Hook &mid = Hook()) {
   constexpr int NW = NT / 32;
@@ -267,7 +271,21 @@ __device__ __forceinline__ void multi_tree_reduce(E (&v)[P], int nparts, E *sred
       const E rhs = upper ? acc : o;
       acc = absorb ? eadd(lhs, rhs) : lhs;
     }
-    if (jl == 0 && c < P) so[c] = acc;
+    if constexpr (FOLD > 0) {
+      // every lane of a column group holds its total; combine the groups
+#pragma unroll
+      for (int f = 1; f < P; f <<= 1) {
+        const E o = eshfl_xor(acc, f * LPC);
+        const bool upper = (c & f) != 0;
+        const bool absorb = ((c & ~(2 * f - 1)) + f) < FOLD;
+        const E lhs = upper ? o : acc;
+        const E rhs = upper ? acc : o;
+        acc = absorb ? eadd(lhs, rhs) : lhs;
+      }
+      if (lane == 0) so[0] = acc;
+    } else {
+      if (jl == 0 && c < P) so[c] = acc;
+    }
   }
   __syncthreads();
   par ^= 1;

@@ -902,8 +902,13 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // block sums of NQ aligned 256-row blocks (reduce-scatter), then their
 // pairwise tree (absorb rule over the blocks)
 template <class T, int P, int NQ, int NT, class Hook = NoHook>
-__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par, const Hook &mid = Hook()) {
+__device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par, bool fold,
+                                            const Hook &mid = Hook()) {
   const T *res = out + par * P;
+  if (fold) {
+    multi_tree_reduce<T, P, NT, NQ>(v, NT, part, out, par, mid);
+    return res[0];
+  }
   multi_tree_reduce<T, P, NT>(v, NT, part, out, par, mid);
   T acc = res[0];
   if constexpr (NQ == 2) acc = eadd(res[0], res[1]);
@@ -929,6 +934,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   __shared__ __align__(8) uint64_t bar[4];     // col0, col1, q0, q1
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const uint32_t cbytes = (uint32_t)m * es * sizeof(double);
+  // warp 0 folds the block sums (dd: cdd factorisation 15.9 -> 15.67 ms);
+  // complex double keeps the per-thread fold (5.05 -> 5.15 ms with warp 0's
+  // two extra shuffle levels on its pivot chain), profiles/r02/exp ab17/ab18
+  constexpr bool fold = Traits<E>::nc >= 2;
   int par = 0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -943,7 +952,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     Rl v[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) v[q] = q < NQ ? eabs2(a[q]) : ezero<Rl>();
-    return fsqrt(pipe_block_sum<Rl, P, NQ, NT>(v, s_pr, s_or, par));
+    return fsqrt(pipe_block_sum<Rl, P, NQ, NT>(v, s_pr, s_or, par, fold));
   };
   // initial column norms of the owned columns (mgs.py:171-172)
   for (int j = cta; j < n; j += G) {
@@ -1072,7 +1081,7 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       const auto mid = [&]() {
         if ((late & 1) && pf && tid == 0) issue_col(jn, s ^ 1);
       };
-      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par, mid);
+      const E r = pipe_block_sum<E, P, NQ, NT>(v, s_pe, s_oe, par, fold, mid);
       double *col = A + (long long)j * m * es;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
