@@ -996,8 +996,12 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     if (!pivot(0, a)) return;
   }
   auto first_after = [&](int k) { return k + 1 + (((cta - (k + 1)) % G) + G) % G; };
+  // No proxy fence at the issue: every generic write of A and Q is followed
+  // by its writer's own fence.proxy.async (after the column update, before a
+  // pivot's publish) and a barrier or release/acquire separates it from the
+  // bulk copy, so a fence here would only stall thread 0 -- and with it warp
+  // 0's part of the reduction the other warps wait for (ncu: barrier stalls)
   auto issue_col = [&](int j, int b) {  // thread 0
-    fence_proxy_async();
     mbar_expect_tx(&bar[b], cbytes);
     bulk_g2s(colb + (size_t)b * m, A + (long long)j * m * es, cbytes, &bar[b]);
   };
@@ -1006,7 +1010,6 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   int qs = 0;      // q buffer of the current sweep
   int qpre = -1;   // (thread 0) sweep whose q is already being copied into the other buffer
   auto issue_q = [&](int k, int b) {  // thread 0
-    fence_proxy_async();
     mbar_expect_tx(&bar[2 + b], cbytes);
     bulk_g2s(qbuf + (size_t)b * m, Q + (long long)k * m * es, cbytes, &bar[2 + b]);
   };
