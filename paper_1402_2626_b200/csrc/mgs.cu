@@ -1554,135 +1554,21 @@ void mgs_impl(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStr
   }
 }
 
-// Blocked back substitution over 32-row diagonal blocks, bottom to top
-// (cooperative launch, one grid barrier per block).  Warp 0 of CTA 0 solves
-// the diagonal block (lane l holds row lo+l; x_j is a shuffle broadcast) and
-// then applies the freshly solved x to the next block's rows itself; all other
-// rows above are updated by the rest of the grid, one thread per row.  Every
-// row still receives its subtractions in descending column order, so x is
-// bit-identical to the reference's sequential solve (mgs.py:229-247).
-// The solver's operands (the diagonal block, the block above it and the
-// hoisted reciprocals) are staged in shared memory with all loads in flight
-// at once, so the sequential chain never waits on L2.
-template <class E, int NT>
-__global__ void __launch_bounds__(NT) k_backsub_blocked(const double *__restrict__ R, int n, double *__restrict__ x,
-                                                        RDiv<Traits<E>::nc> *__restrict__ prep,
-                                                        double *__restrict__ y, int *sing, MgsStatus *status,
-                                                        int unroll) {
-  namespace cg = cooperative_groups;
-  using RD = RDiv<Traits<E>::nc>;
-  constexpr int es = Traits<E>::es;
-  extern __shared__ __align__(16) double bs_smem[];
-  E *sD = reinterpret_cast<E *>(bs_smem);  // 32 x 32 diagonal block, column-major
-  E *sU = sD + 32 * 32;                     // 32 x 32 block above it (rows lo-32..lo-1)
-  E *sX = sU + 32 * 32;                     // x of the current block
-  RD *sP = reinterpret_cast<RD *>(sX + 32);
-  cg::grid_group grid = cg::this_grid();
-  if (status->code) return;  // the factorisation failed (uniform for all CTAs)
-  const long long ld = n + 1;
-  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
-  for (int j = gtid; j < n; j += gsize) {
-    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
-    const double *dg = R + ((long long)j * ld + j) * es;
-    bool nz = false;
-#pragma unroll
-    for (int p = 0; p < es; ++p) nz |= dg[p] != 0.0;
-    if (!nz) atomicMax(sing, j);
-    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
-  }
-  grid.sync();
-  if (*(volatile int *)sing >= 0) {
-    if (gtid == 0) {
-      status->k = *sing;
-      status->code = PN_E_SINGULAR;
-    }
-    return;
-  }
-  const bool solver = blockIdx.x == 0 && threadIdx.x < 32;
-  const int lane = threadIdx.x & 31;
-  const int nb = (n + 31) / 32;
-  E yr = ezero<E>();  // solver lane's row of the current diagonal block
-  if (solver) {
-    const int r = (nb - 1) * 32 + lane;
-    if (r < n) yr = eload<E>(y + (long long)r * es);
-  }
-  for (int b = nb - 1; b >= 0; --b) {
-    const int lo = b * 32, hi = min(n, lo + 32);
-    if (solver) {
-      // stage the diagonal block (rows lo..j of column j) and the reciprocals
-      for (int jj = 0; jj < hi - lo; ++jj)
-        if (lane <= jj) sD[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + lo + lane) * es);
-      if (lo + lane < hi) sP[lane] = prep[lo + lane];
-      __syncwarp();
-      E xl = ezero<E>();
-      for (int j = hi - 1; j >= lo; --j) {
-        const int jl = j - lo;
-        if (lane == jl) xl = ediv_with(yr, sD[jl * 32 + jl], sP[jl]);
-        const E xj = eshfl_idx(xl, jl);
-        if (lane < jl) yr = esub(yr, emul(sD[jl * 32 + lane], xj));
-      }
-      if (lo + lane < hi) {
-        estore(x + (long long)(lo + lane) * es, xl);
-        sX[lane] = xl;
-      }
-      __syncwarp();
-    }
-    grid.sync();
-    if (b == 0) break;
-    // rows of block b-1 (solver warp) and all rows above it (rest of the grid)
-    if (solver) {
-      const int r = lo - 32 + lane;
-      for (int jj = 0; jj < hi - lo; ++jj) sU[jj * 32 + lane] = eload<E>(R + ((long long)(lo + jj) * ld + r) * es);
-      yr = eload<E>(y + (long long)r * es);
-      __syncwarp();
-      if (unroll) {
-        const int nbk = hi - lo;
-#pragma unroll 8
-        for (int jj = 31; jj >= 0; --jj)
-          if (jj < nbk) yr = esub(yr, emul(sU[jj * 32 + lane], sX[jj]));
-      } else {
-        for (int j = hi - 1; j >= lo; --j) yr = esub(yr, emul(sU[(j - lo) * 32 + lane], sX[j - lo]));
-      }
-    } else {
-      const int worker = blockIdx.x == 0 ? threadIdx.x - 32 : gtid - 32;
-      const int workers = gsize - 32;
-      for (int r = worker; r < lo - 32; r += workers) {
-        E v = eload<E>(y + (long long)r * es);
-        if (unroll) {
-          const int nbk = hi - lo;
-#pragma unroll 4
-          for (int jj = 31; jj >= 0; --jj)
-            if (jj < nbk)
-              v = esub(v, emul(eload<E>(R + ((long long)(lo + jj) * ld + r) * es), eload<E>(x + (long long)(lo + jj) * es)));
-          estore(y + (long long)r * es, v);
-          continue;
-        }
-        E rn = eload<E>(R + ((long long)(hi - 1) * ld + r) * es);
-        for (int j = hi - 1; j >= lo; --j) {
-          const E rc = rn;
-          if (j > lo) rn = eload<E>(R + ((long long)(j - 1) * ld + r) * es);
-          v = esub(v, emul(rc, eload<E>(x + (long long)j * es)));
-        }
-        estore(y + (long long)r * es, v);
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
-// Lane-parallel back substitution for complex quad double.  The solve is a
-// chain of n dependent complex-qd operations; a single lane issues a complex
-// multiply in ~4300 cycles (profiles/r01/micro_fp64.txt) because its four
-// qd products share one instruction stream.  Here four lanes own a row and
+// Back substitution R x = y, y = R[:n, n] (mgs.py:229-247), over 32-row
+// diagonal blocks from the bottom, one cooperative launch with one grid
+// barrier per block.  Every row receives its subtractions in descending
+// column order, so x is bit-identical to the reference's sequential solve.
+//
+// Lane-parallel arithmetic for complex quad double: the solve is a chain of
+// n dependent complex-qd operations; a single lane issues a complex multiply
+// in ~4300 cycles (profiles/r01/micro_fp64.txt) because its four qd products
+// share one instruction stream.  In k_backsub_look four lanes own a row and
 // compute the four real products of every complex multiply side by side
 // (then two lanes form re = t1 - t2 and im = t3 + t4), which shortens the
 // chain about 2.5x.  The reference's operation sequence is unchanged
-// (xprec.py:302-306, varith.py:130-136), so x is bit-identical.
-//
-// Layout: CTA 0 (128 threads = 32 rows x 4 lanes) solves each 32-row
-// diagonal block and then applies the block's x to the next block's rows;
-// the rest of the grid updates all rows above that, one lane per row, with
-// one grid barrier per block (as k_backsub_blocked).
+// (xprec.py:302-306, varith.py:130-136).
 
 template <int NC>
 __device__ __forceinline__ F<NC> shfl_fn(const F<NC> &v, int src) {
@@ -1724,120 +1610,18 @@ __device__ __forceinline__ C<NC> lp_div(const C<NC> &yv, const C<NC> &r, const R
   return {shfl_fn(v, g4), shfl_fn(v, g4 + 1)};
 }
 
-template <int NC, int NT>
-__global__ void __launch_bounds__(NT) k_backsub_lanes(const double *__restrict__ R, int n, double *__restrict__ x,
-                                                      RDiv<NC> *__restrict__ prep, double *__restrict__ y,
-                                                      int *sing, MgsStatus *status, int unroll) {
-  namespace cg = cooperative_groups;
-  using E = C<NC>;
-  constexpr int es = 2 * NC;
-  static_assert(NT == 128, "CTA 0 is 32 rows x 4 lanes");
-  extern __shared__ __align__(16) double bl_smem[];
-  E *sD = reinterpret_cast<E *>(bl_smem);  // 32 x 32 diagonal block, column-major
-  E *sU = sD + 32 * 32;                     // 32 x 32 block above it
-  E *sX = sU + 32 * 32;                     // x of the current block
-  RDiv<NC> *sP = reinterpret_cast<RDiv<NC> *>(sX + 32);
-  cg::grid_group grid = cg::this_grid();
-  if (status->code) return;
-  const long long ld = n + 1;
-  const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
-  for (int j = gtid; j < n; j += gsize) {
-    estore(y + (long long)j * es, eload<E>(R + ((long long)n * ld + j) * es));
-    const double *dg = R + ((long long)j * ld + j) * es;
-    bool nz = false;
-#pragma unroll
-    for (int q = 0; q < es; ++q) nz |= dg[q] != 0.0;
-    if (!nz) atomicMax(sing, j);
-    else prep[j] = rdiv_prepare(ediv_den(eload<E>(dg)));
-  }
-  grid.sync();
-  if (*(volatile int *)sing >= 0) {
-    if (gtid == 0) {
-      status->k = *sing;
-      status->code = PN_E_SINGULAR;
-    }
-    return;
-  }
-  const bool solver = blockIdx.x == 0;
-  const int t = threadIdx.x, lane = t & 31, p = lane & 3, g4 = lane & ~3;
-  const int rl = t >> 2;  // solver row within the block
-  const int nb = (n + 31) / 32;
-  for (int b = nb - 1; b >= 0; --b) {
-    const int lo = b * 32, hi = min(n, lo + 32), nbk = hi - lo;
-    if (solver) {
-      for (int e = t; e < 32 * 32; e += NT) {
-        const int jj = e >> 5, ii = e & 31;
-        if (jj < nbk && ii <= jj) sD[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo + ii) * es);
-      }
-      if (t < nbk) sP[t] = prep[lo + t];
-      __syncthreads();
-      E yr = rl < nbk ? eload<E>(y + (long long)(lo + rl) * es) : ezero<E>();
-      for (int j = hi - 1; j >= lo; --j) {
-        const int jl = j - lo;
-        if ((jl >> 3) == (t >> 5)) {  // the warp holding row jl divides (all its lanes shuffle)
-          const E xj = lp_div(yr, sD[jl * 32 + jl], sP[jl], p, g4);
-          if (rl == jl && p == 0) sX[jl] = xj;
-        }
-        __syncthreads();
-        if ((t >> 5) * 8 < jl) {  // warps with a row below jl update
-          const E u = lp_csub(yr, lp_cmul(sD[jl * 32 + rl], sX[jl], p, g4), p, g4);
-          if (rl < jl) yr = u;
-        }
-      }
-      __syncthreads();
-      if (t < nbk) estore(x + (long long)(lo + t) * es, sX[t]);
-    }
-    grid.sync();  // x of block b is visible to every CTA
-    if (b == 0) break;
-    if (solver) {
-      // the next block's rows take this block's x, in descending column order
-      const int r = lo - 32 + rl;
-      for (int e = t; e < 32 * 32; e += NT) {
-        const int jj = e >> 5, ii = e & 31;
-        if (jj < nbk) sU[e] = eload<E>(R + ((long long)(lo + jj) * ld + lo - 32 + ii) * es);
-      }
-      __syncthreads();
-      E v = eload<E>(y + (long long)r * es);
-      // unrolled: the products are independent of v, only the subtractions
-      // chain (PN_BACKSUB_UNROLL=0: the plain loop, for comparison)
-      if (unroll) {
-#pragma unroll 8
-        for (int jj = 31; jj >= 0; --jj)
-          if (jj < nbk) v = lp_csub(v, lp_cmul(sU[jj * 32 + rl], sX[jj], p, g4), p, g4);
-      } else {
-        for (int j = hi - 1; j >= lo; --j) v = lp_csub(v, lp_cmul(sU[(j - lo) * 32 + rl], sX[j - lo], p, g4), p, g4);
-      }
-      if (p == 0) estore(y + (long long)r * es, v);
-      __syncthreads();
-    } else {
-      // all rows above the next block take this block's x
-      for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {
-        E v = eload<E>(y + (long long)r * es);
-        if (unroll) {
-#pragma unroll 4
-          for (int jj = 31; jj >= 0; --jj)
-            if (jj < nbk)
-              v = esub(v, emul(eload<E>(R + ((long long)(lo + jj) * ld + r) * es), eload<E>(x + (long long)(lo + jj) * es)));
-        } else {
-          for (int j = hi - 1; j >= lo; --j)
-            v = esub(v, emul(eload<E>(R + ((long long)j * ld + r) * es), eload<E>(x + (long long)j * es)));
-        }
-        estore(y + (long long)r * es, v);
-      }
-    }
-  }
-}
 
-// k_backsub_look: k_backsub_lanes with the next block's rows updated inside
-// the solve.  CTA 0 has two 128-thread groups: the solver (rows of block b,
+// k_backsub_look (complex qd): CTA 0 has two 128-thread groups: the solver
+// (rows of block b,
 // four lanes per row) and a lookahead group holding the 32 rows of block b-1,
 // which subtracts R[i, j] x_j for each x_j of block b as soon as the solver
 // has it (two updates per solver step), after first catching up on block
 // b+1's x.  The other CTAs apply block b+1's x to every row below block b-1
 // meanwhile.  Every row still takes its updates in descending j (blocks b+2..
 // from the other CTAs in earlier rounds, then b+1 and b from the lookahead
-// group), so x is bit-identical to k_backsub_lanes; the solver no longer
-// waits for a separate next-block pass (mgs.py:229-247).
+// group); the solver never waits for a separate next-block pass
+// (mgs.py:229-247).  (The plain lanes kernel without the lookahead group:
+// 5.2 vs 3.7 ms at n = 1024, removed.)
 template <int NC>
 __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__ R, int n, double *__restrict__ x,
                                                       RDiv<NC> *__restrict__ prep, double *__restrict__ y,
@@ -1964,11 +1748,13 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
   }
 }
 
-// k_backsub_blocked_look: k_backsub_blocked (one lane per row) with the
+// k_backsub_blocked_look (d, dd, real qd): one lane per row with the
 // lookahead of k_backsub_look: warp 0 of CTA 0 solves block b, warp 1 holds
 // block b-1's rows, applies block b+1's x and then block b's x_j as warp 0
 // publishes them; the rest of the grid applies block b+1's x to the rows
-// below block b-1.  Same per-row subtraction order as k_backsub_blocked.
+// below block b-1.  The solver's operands (diagonal block, the blocks above
+// it, the hoisted reciprocals) are staged in shared memory with all loads in
+// flight at once, so the sequential chain never waits on L2.
 template <class E, int NT>
 __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__restrict__ R, int n,
                                                              double *__restrict__ x,
@@ -2070,13 +1856,14 @@ template <class E>
 void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st) {
   constexpr int es = Traits<E>::es;
   DevBuf prep((size_t)n * Traits<E>::nc * sizeof(double) + 16, st);
+  // PN_BACKSUB_MODE=single: one CTA, n <= 1024 (tests); default: lookahead
   const char *mode = getenv("PN_BACKSUB_MODE");
-  // complex qd: four lanes per row (default).  Complex dd measured slower
-  // with lanes (1.18 vs 1.0 ms at n = 1024): its chain is short already.
+  const bool look = !(mode && strcmp(mode, "single") == 0);
+  // complex qd: four lanes per row.  Complex dd measured slower with lanes
+  // (1.18 vs 1.0 ms at n = 1024): its chain is short already.
   if constexpr (Traits<E>::cplx && Traits<E>::nc == 4) {
     constexpr int NC = Traits<E>::nc;
-    // default: the lookahead kernel (3.7 vs 5.2 ms for lanes at n = 1024)
-    if (!mode || strcmp(mode, "look") == 0) {
+    if (look) {
       constexpr int NT = 256;
       DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
       DevBuf sbuf(16, st);
@@ -2093,28 +1880,8 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
       count_launch(1);
       return;
     }
-    if (strcmp(mode, "lanes") == 0) {
-      constexpr int NT = 128;
-      DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
-      DevBuf sbuf(16, st);
-      int *sing = sbuf.as<int>();
-      PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
-      const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
-      RDiv<NC> *pp = prep.as<RDiv<NC>>();
-      double *yp = yw.d();
-      MgsStatus *status = w.status.as<MgsStatus>();
-      const char *uv = getenv("PN_BACKSUB_UNROLL");
-      int unroll = uv ? atoi(uv) : 1;
-      void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status, &unroll};
-      const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<NC>);
-      PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_lanes<NC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-      PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_lanes<NC, NT>, grid, NT, args, smem, st));
-      count_launch(1);
-      return;
-    }
   }
-  if (!mode || strcmp(mode, "look") == 0) {
+  if (look) {
     constexpr int NT = 128;
     DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
     DevBuf sbuf(16, st);
@@ -2129,26 +1896,6 @@ void backsub_impl(int n, const double *R, double *x, MgsWork &w, cudaStream_t st
     auto kern = k_backsub_blocked_look<E, NT>;
     PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)kern, grid, NT, args, smem, st));
-    count_launch(1);
-    return;
-  }
-  if (!(mode && strcmp(mode, "single") == 0)) {
-    constexpr int NT = 128;
-    DevBuf yw((size_t)n * es * sizeof(double) + 16, st);
-    DevBuf sbuf(16, st);
-    int *sing = sbuf.as<int>();
-    PN_CHECK_CUDA(cudaMemsetAsync(sing, 0xff, sizeof(int), st));
-    const int grid = std::max(2, std::min(num_sms(), (n + NT - 1) / NT + 1));
-    RDiv<Traits<E>::nc> *pp = prep.as<RDiv<Traits<E>::nc>>();
-    double *yp = yw.d();
-    MgsStatus *status = w.status.as<MgsStatus>();
-    const char *uv = getenv("PN_BACKSUB_UNROLL");
-    int unroll = uv ? atoi(uv) : 1;
-    void *args[] = {(void *)&R, &n, &x, &pp, &yp, &sing, &status, &unroll};
-    const size_t smem = (size_t)(2 * 32 * 32 + 32) * es * sizeof(double) + 32 * sizeof(RDiv<Traits<E>::nc>);
-    PN_CHECK_CUDA(cudaFuncSetAttribute(k_backsub_blocked<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    PN_CHECK_CUDA(cudaLaunchCooperativeKernel((const void *)k_backsub_blocked<E, NT>, grid, NT, args, smem, st));
     count_launch(1);
     return;
   }
