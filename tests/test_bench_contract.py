@@ -78,3 +78,40 @@ def test_oracle_generator_matches_product_generator():
         for a, b in ((p.poly_ptr, c.poly_ptr), (p.mon_ptr, c.mon_ptr), (p.var_idx, c.var_idx), (p.exps, c.exps),
                      (p.coeffs, c.coeffs)):
             assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+REDUCE_PROBE = """
+import os, sys, json
+import torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+import bench
+dist.init_process_group("gloo")
+r = dist.get_rank()
+mx = bench.reduce_ranks([1.0 + r, 10.0 - r], "max")
+sm = bench.reduce_ranks([1.0 + r], "sum")
+print(json.dumps({"rank": r, "max": mx, "sum": sm}))
+dist.destroy_process_group()
+"""
+
+
+def test_max_over_ranks_gloo_world2(tmp_path):
+    """The timing reductions of an N-rank bench run (max of the elapsed times,
+    sum of the work) over two gloo ranks (PN_BENCH_SHARED_GPU: host tensors)."""
+    probe = tmp_path / "probe.py"
+    probe.write_text(REDUCE_PROBE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(probe)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={**os.environ, "PN_BENCH_SHARED_GPU": "1", "OMP_NUM_THREADS": "1"})
+    assert out.returncode == 0, out.stderr[-2000:]
+    recs = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(r["rank"] for r in recs) == [0, 1]
+    for r in recs:
+        assert r["max"] == [2.0, 10.0] and r["sum"] == [3.0]
+
+
+def _port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
