@@ -35,7 +35,7 @@ def main(src, dst, tag):
         out[f"{kernel} | {workload}"] = {
             "dram_read_bytes": rd, "dram_write_bytes": wr,
             "duration": f"{d['gpu__time_duration.sum']} {u['gpu__time_duration.sum']}",
-            "source": f"ncu --set full, profiles/{tag}/{name}_details.csv"}
+            "source": f"ncu --set full, profiles/{tag}/final/raw/{name}_raw.csv"}
     json.dump(out, open(dst, "w"), indent=1)
 
 
