@@ -3,6 +3,7 @@
 // mgs.cu, compiled once per precision level).
 #include "common.cuh"
 #include "internal.h"
+#include "nvtx.h"
 
 namespace pn {
 
@@ -63,6 +64,7 @@ using namespace pn;
 
 extern "C" int pn_evaldiff(pn_system *sys, const double *x, double *f, double *J, pn_counts *counts, void *stream) {
   PN_API_BEGIN
+  NvtxRange range("pn_evaldiff");
   PN_REQUIRE(sys && x, PN_E_ARG, "pn_evaldiff: NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   const int es = sys->es, m = sys->m, n = sys->n;
@@ -94,6 +96,7 @@ struct LsqBuffers {
 extern "C" int pn_mgs_qr(int nc, int cplx, int32_t m, int32_t n, const double *aug, double *Q, double *R,
                          pn_numinfo *info, void *stream) {
   PN_API_BEGIN
+  NvtxRange range("pn_mgs_qr");
   check_level(nc, cplx);
   PN_REQUIRE(aug, PN_E_ARG, "pn_mgs_qr: aug is NULL");
   PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
@@ -146,6 +149,7 @@ extern "C" int pn_back_substitute(int nc, int cplx, int32_t n, const double *R, 
 extern "C" int pn_least_squares(int nc, int cplx, int32_t m, int32_t n, const double *aug, double *x, double *z,
                                 double *Q, double *R, pn_numinfo *info, void *stream) {
   PN_API_BEGIN
+  NvtxRange range("pn_least_squares");
   check_level(nc, cplx);
   PN_REQUIRE(aug && x, PN_E_ARG, "pn_least_squares: NULL argument");
   PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);

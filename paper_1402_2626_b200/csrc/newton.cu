@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "nvtx.h"
 
 using namespace pn;
 
@@ -63,6 +64,7 @@ static void capture_step_graph(pn_system *sys, F &&device_step) {
 extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, double *f, double *dx,
                               double *fmod, double *dxmod, double *xmod, pn_numinfo *info, void *stream) {
   PN_API_BEGIN
+  NvtxRange range("pn_newton_step");
   PN_REQUIRE(sys && x, PN_E_ARG, "pn_newton_step: NULL argument");
   const int m = sys->m, n = sys->n, es = sys->es, nc = sys->nc, cplx = sys->cplx;
   PN_REQUIRE(m >= n && n >= 1, PN_E_ARG, "need m >= n >= 1, got m=%d, n=%d", m, n);
@@ -90,11 +92,20 @@ extern "C" int pn_newton_step(pn_system *sys, const double *x, double *x_next, d
     };
     rec(e[0]);
     // A = J(x) with b = -f(x) in column n (newton.py:84-87)
-    evaldiff_device(sys, xa, fa, A, m, n, s);
+    {
+      NvtxRange r("evaluate");
+      evaldiff_device(sys, xa, fa, A, m, n, s);
+    }
     rec(e[1]);
-    mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, s);
+    {
+      NvtxRange r("factor");
+      mgs_factor_device(nc, cplx, m, n, A, Q, R, sys->mgs, s);
+    }
     rec(e[4]);
-    backsub_device(nc, cplx, n, R, dxa, sys->mgs, s);
+    {
+      NvtxRange r("back_substitute");
+      backsub_device(nc, cplx, n, R, dxa, sys->mgs, s);
+    }
     rec(e[2]);
     // x_next = x + dx (newton.py:92)
     vec_op_aos(nc, cplx, PN_OP_ADD, n, xa, dxa, xn, s);
@@ -235,6 +246,7 @@ double host_inf_norm(const std::vector<double> &mod, int nc, int len) {
 static void newton_batch_serial(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
                                 double tol, double *x_out, int32_t *iters, int32_t *status, cudaStream_t st,
                                 const DevBuf &cpos_d) {
+  NvtxRange range("newton_batch_serial");
   PN_REQUIRE(sys && x0 && x_out && iters && status && B >= 0 && max_iters >= 1, PN_E_ARG,
              "pn_newton_batch: bad arguments");
   const int m = sys->m, n = sys->n, es = sys->es, nc = sys->nc, cplx = sys->cplx;
@@ -390,6 +402,7 @@ static void batch_alloc(pn_system *sys, BatchSlots &s, int W, cudaStream_t st) {
 extern "C" int pn_newton_batch(pn_system *sys, int64_t B, const double *x0, const double *consts, int max_iters,
                                double tol, double *x_out, int32_t *iters, int32_t *status, void *stream) {
   PN_API_BEGIN
+  NvtxRange range("pn_newton_batch");
   PN_REQUIRE(sys && x0 && x_out && iters && status && B >= 0 && max_iters >= 1, PN_E_ARG,
              "pn_newton_batch: bad arguments");
   const int m = sys->m, n = sys->n, es = sys->es;
