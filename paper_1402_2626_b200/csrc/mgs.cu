@@ -1500,6 +1500,14 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     if constexpr (B == 8) {
       if (m <= 1536 && flow_launch<E, B, 192>(m, n, A, Q, R, w, st)) return;
     }
+    // real qd, 2048 < m <= 4096 (Chandrasekhar real qd): the column fills
+    // one CTA's shared memory either way; 16 warps x 8 rows instead of 8 x 16
+    // (PN_FLOW_WIDE=0 keeps the 256-thread CTA)
+    if constexpr (B == 16 && !Traits<E>::cplx) {
+      const char *fw = getenv("PN_FLOW_WIDE");
+      const bool wide = fw ? strcmp(fw, "0") != 0 : true;
+      if (wide && m > 2048 && flow_launch<E, 8, 512>(m, n, A, Q, R, w, st)) return;
+    }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
   }
   // d/dd columns of 2048 < m <= 4096 rows: the flow kernel with 1024-thread
