@@ -1494,6 +1494,16 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     }
     if (done) return;
   }
+  // complex dd with 1024 < m <= 2048 rows: the flow kernel (8 rows per
+  // thread, two CTAs per SM) instead of the dataflow kernel: factorisation
+  // 80.3 -> 57.3 ms at 1536 rows, 153 -> 115 ms at 2048, Chandrasekhar
+  // n = 2048 cdd (6 steps) 0.944 -> 0.718 s; complex double stays on the
+  // dataflow kernel (24.3 vs 29.5 ms at 1536), above 2048 rows the wide flow
+  // kernel wins (profiles/r02/exp ab43/ab44).  PN_FLOW_TALL=0 keeps dataflow.
+  if (mode == 4 && Traits<E>::nc == 2 && Traits<E>::cplx && m > 1024 && m <= 2048) {
+    const char *ft = getenv("PN_FLOW_TALL"), *fw = getenv("PN_FLOW_WIDE");
+    if (!(ft && strcmp(ft, "0") == 0) && !(fw && strcmp(fw, "1") == 0)) mode = 0;
+  }
   if (mode == 0) {
     // 6 warps x 8 rows for 1024 < m <= 1536 (the C4 overdetermined shape):
     // a 96 KB column, two CTAs per SM instead of one 128 KB CTA

@@ -269,3 +269,19 @@ def test_tall_least_squares_wide_flow_vs_oracle(gpu, monkeypatch, lv, m, n, wide
     assert same(res.factors.Q, Q)
     assert same(res.x, x)
     assert res.z == z
+
+@pytest.mark.parametrize("lv,m,n", [("cdd", 1600, 120), ("cdd", 1536, 70), ("cdd", 2048, 40)])
+@pytest.mark.parametrize("tall", ["1", "0"])
+def test_mid_tall_cdd_flow_vs_oracle(gpu, monkeypatch, lv, m, n, tall):
+    """complex dd with 1024 < m <= 2048 rows: the flow kernel (default,
+    PN_FLOW_TALL) and the dataflow kernel, against the oracle."""
+    from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
+    from paper_1402_2626_b200.varith import VecContext
+    monkeypatch.setenv("PN_FLOW_TALL", tall)
+    L, aug = _busy_aug(lv, m, n, m + 3 * n)
+    res = least_squares_solve(AugmentedMatrix(VecContext(level_from_name(lv)), aug))
+    x, z, Q, R = oracle.least_squares(L, aug, nthreads=NT)
+    assert same(res.factors.R, R)
+    assert same(res.factors.Q, Q)
+    assert same(res.x, x)
+    assert res.z == z
