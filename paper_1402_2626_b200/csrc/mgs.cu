@@ -1513,7 +1513,7 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     // real qd, 2048 < m <= 4096 (Chandrasekhar real qd): the column fills
     // one CTA's shared memory either way; 16 warps x 8 rows instead of 8 x 16
     // (PN_FLOW_WIDE=0 keeps the 256-thread CTA)
-    if constexpr (B == 16 && !Traits<E>::cplx) {
+    if constexpr (B == 16 && Traits<E>::nc == 4 && !Traits<E>::cplx) {
       const char *fw = getenv("PN_FLOW_WIDE");
       const bool wide = fw ? strcmp(fw, "0") != 0 : true;
       if (wide && m > 2048 && flow_launch<E, 8, 512>(m, n, A, Q, R, w, st)) return;
@@ -1523,11 +1523,17 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
   // d/dd columns of 2048 < m <= 4096 rows: the flow kernel with 1024-thread
   // CTAs (4 rows per thread, the working column in shared memory, one CTA
   // per SM) instead of the streaming dataflow kernel -- Chandrasekhar
-  // n = 4096 cdd, 6 Newton steps 9.9 -> 6.2 s (equal at 2048).
-  // PN_FLOW_WIDE=0|1 forces it off / on for 1024 < m <= 4096.
+  // n = 4096 cdd, 6 Newton steps 9.9 -> 6.2 s (equal at 2048).  Complex dd:
+  // 512 threads x 8 rows (128 registers instead of 64): factorisation 3072
+  // rows 431.7 -> 408.6 ms, 4096 rows 951 -> 890 ms; complex double keeps
+  // 1024 x 4 (154.6 vs 212.8 ms at 3072; profiles/r02/exp ab46).
+  // PN_FLOW_WIDE=0|1|2 forces dataflow / 1024 threads / 512 threads.
   if (mode == 4 && Traits<E>::nc <= 2 && m > 1024 && m <= 4096) {
     const char *fw = getenv("PN_FLOW_WIDE");
-    const bool wide = fw ? strcmp(fw, "1") == 0 : m > 2048;
+    const int wide = fw ? atoi(fw) : (m > 2048 ? (Traits<E>::nc == 2 && Traits<E>::cplx ? 2 : 1) : 0);
+    if constexpr (B == 16 && Traits<E>::nc == 2) {
+      if (wide == 2 && flow_launch<E, 8, 512>(m, n, A, Q, R, w, st)) return;
+    }
     if (wide && flow_launch<E, 4, 1024>(m, n, A, Q, R, w, st)) return;
   }
   if (mode <= 1 || mode == 4) {

@@ -253,12 +253,12 @@ def test_cyclic_300_all_large_buckets_vs_oracle(gpu, monkeypatch, lv, warp):
 
 @pytest.mark.parametrize("lv,m,n", [("cdd", 4096, 48), ("cd", 3000, 200), ("rdd", 2100, 130), ("rqd", 4064, 40),
                                     ("rqd", 2100, 90)])
-@pytest.mark.parametrize("wide", ["1", "0"])
+@pytest.mark.parametrize("wide", ["2", "1", "0"])
 def test_tall_least_squares_wide_flow_vs_oracle(gpu, monkeypatch, lv, m, n, wide):
-    """1024 < m <= 4096 rows: d/dd take the 1024-thread flow kernel (default
-    above 2048 rows, PN_FLOW_WIDE) or the dataflow kernel, real qd the
-    512-thread flow kernel or the 256-thread one, against the oracle (the
-    shapes of the Chandrasekhar n = 2048..4096 runs)."""
+    """1024 < m <= 4096 rows: d/dd take the 512-thread (dd) or 1024-thread
+    flow kernel (default above 2048 rows, PN_FLOW_WIDE) or the dataflow
+    kernel, real qd the 512-thread flow kernel or the 256-thread one, against
+    the oracle (the shapes of the Chandrasekhar n = 2048..4096 runs)."""
     from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
     from paper_1402_2626_b200.varith import VecContext
     monkeypatch.setenv("PN_FLOW_WIDE", wide)
