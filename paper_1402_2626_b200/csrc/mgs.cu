@@ -934,10 +934,11 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   __shared__ __align__(8) uint64_t bar[4];     // col0, col1, q0, q1
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const uint32_t cbytes = (uint32_t)m * es * sizeof(double);
-  // warp 0 folds the block sums (dd: cdd factorisation 15.9 -> 15.67 ms);
-  // complex double keeps the per-thread fold (5.05 -> 5.15 ms with warp 0's
-  // two extra shuffle levels on its pivot chain), profiles/r02/exp ab17/ab18
-  constexpr bool fold = Traits<E>::nc >= 2;
+  // warp 0 folds the block sums (dd at m = 1024: cdd factorisation 15.9 ->
+  // 15.67 ms); complex double keeps the per-thread fold (5.05 -> 5.15 ms with
+  // warp 0's two extra shuffle levels on its pivot chain), and so do fewer
+  // than four blocks (0.5 % at m = 512 / 768), profiles/r02/exp ab17/ab18/ab52
+  constexpr bool fold = Traits<E>::nc >= 2 && NQ == 4;
   int par = 0;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -1357,11 +1358,13 @@ static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
   int *ready = w.ready.as<int>();
   // PN_PIPE_LATE bit 0: late prefetch (no closing barrier per apply): cdd
-  // factorisation 16.13 -> 15.99 ms; cd 5.05 -> 7.46 ms (its short applies no
-  // longer cover the column copy), so double double only (profiles/r02/exp
-  // ab8/ab9).  Bit 1: the two-barrier pivot wait instead of the one-barrier one.
+  // factorisation 16.13 -> 15.99 ms at m = 1024; but cd 5.05 -> 7.46 ms and
+  // cdd at m = 512 / 768 4.14 -> 5.65 / 9.05 -> 13.94 ms (shorter applies no
+  // longer cover the column copy), so double double with four row blocks
+  // only (profiles/r02/exp ab8/ab9/ab51).  Bit 1: the two-barrier pivot wait
+  // instead of the one-barrier one.
   const char *lv = getenv("PN_PIPE_LATE");
-  int late = lv ? atoi(lv) : (Traits<E>::nc == 2 ? 1 : 0);
+  int late = lv ? atoi(lv) : (Traits<E>::nc == 2 && NQ == 4 ? 1 : 0);
   void *args[] = {&A, &m, &n, &orig, (void *)&eps, &Q, &R, &status, &ready, &late};
   unsigned long long *tr = nullptr;
   trace_begin(n, &tr);
