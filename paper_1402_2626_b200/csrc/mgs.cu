@@ -917,7 +917,54 @@ __device__ __forceinline__ T pipe_block_sum(T (&v)[P], T *part, T *out, int &par
   return acc;
 }
 
-template <class E, int NQ, int QB>
+// thread-block cluster helpers (the PAIR variant of k_mgs_pipe)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_peer(const void *p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+// one element to the peer's shared memory, completing bytes on its mbarrier
+template <class E>
+__device__ __forceinline__ void st_async_elem(uint32_t addr, const E &v, uint32_t peer_bar) {
+  const double *d = reinterpret_cast<const double *>(&v);
+  constexpr int es = Traits<E>::es;
+  if constexpr (es % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < es; i += 2)
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                       addr + 8 * i),
+                   "d"(d[i]), "d"(d[i + 1]), "r"(peer_bar)
+                   : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < es; ++i)
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(addr + 8 * i),
+                   "d"(d[i]), "r"(peer_bar)
+                   : "memory");
+  }
+}
+__device__ __forceinline__ void remote_arrive(uint32_t peer_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(peer_bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ bool mbar_try_cluster(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <class E, int NQ, int QB, bool PAIR = false>
 __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int m, int n, double *__restrict__ orig,
                                                      double eps, double *__restrict__ Q, double *__restrict__ R,
                                                      MgsStatus *status, int *ready, int late) {
@@ -929,9 +976,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   extern __shared__ __align__(128) double pipe_smem[];
   E *colb = reinterpret_cast<E *>(pipe_smem);  // [2][m]
   E *qbuf = colb + 2 * m;                      // [QB][m] (QB = 2: q_{k+1} prefetched)
+  E *qd = qbuf + (size_t)QB * m;               // PAIR: q_k pushed by the cluster partner
   __shared__ E s_pe[2 * NW * P], s_oe[2 * P];
   __shared__ Rl s_pr[2 * NW * P], s_or[2 * P];
-  __shared__ __align__(8) uint64_t bar[4];     // col0, col1, q0, q1
+  __shared__ __align__(8) uint64_t bar[6];     // col0, col1, q0, q1; PAIR: q pushed, pair buffer free
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const uint32_t cbytes = (uint32_t)m * es * sizeof(double);
   // warp 0 folds the block sums (dd at m = 1024: cdd factorisation 15.9 ->
@@ -945,10 +993,54 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[3], 1);
+    if (PAIR) {
+      mbar_init(&bar[4], 1);
+      mbar_init(&bar[5], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   uint32_t ph[4] = {0, 0, 0, 0};
+  // PAIR (cluster of two CTAs, 2i and 2i+1): column c of rank 0 is followed
+  // by column c+1 of rank 1, so rank 0 pushes every q_c it pivots straight
+  // into rank 1's shared memory (st.async, completing on rank 1's mbarrier)
+  // and rank 1 starts its pivot sweep without the flag poll and bulk copy
+  uint32_t rank = 0, ph4 = 0, ph5 = 0, peer_qd = 0, peer_b4 = 0, peer_b5 = 0;
+  if constexpr (PAIR) {
+    rank = cluster_rank();
+    peer_qd = map_peer(qd, rank ^ 1);
+    peer_b4 = map_peer(&bar[4], rank ^ 1);
+    peer_b5 = map_peer(&bar[5], rank ^ 1);
+    cluster_sync_all();  // the partner's barriers are initialised
+    if (rank == 1 && tid == 0) remote_arrive(peer_b5);  // the pair buffer starts free
+  }
+  // every exit: no remote operation may target a CTA that has left
+  auto leave = [&]() {
+    if constexpr (PAIR) cluster_sync_all();
+  };
+  __shared__ int s_pok;
+  // thread 0 waits on a cluster-scope mbarrier phase, giving up on a failure
+  // status; the result is broadcast (one barrier)
+  auto wait_cluster_bar = [&](uint64_t *b, uint32_t parity) -> bool {
+    if (tid == 0) {
+      int ok = 1;
+      long long t0 = clock64();
+      while (!mbar_try_cluster(b, parity)) {
+        if (ld_acquire(&status->code) != 0) {
+          ok = 0;
+          break;
+        }
+        if (clock64() - t0 > (1ll << 36)) {
+          atomicExch(&status->code, PN_E_CUDA);
+          ok = 0;
+          break;
+        }
+      }
+      s_pok = ok;
+    }
+    __syncthreads();
+    return s_pok != 0;
+  };
   auto col_norm = [&](const E (&a)[NQ]) -> Rl {
     Rl v[P];
 #pragma unroll
@@ -983,9 +1075,22 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     if (tid == 0) estore(R + ((long long)c * (n + 1) + c) * es, eembed(rkk, (E *)nullptr));
     if (c < n) {
       const RDiv<Traits<E>::nc> p = rdiv_prepare(rkk);
+      E qv[NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) estore(Q + ((long long)c * m + q * NT + tid) * es, ediv_prepared(a[q], p));
+      for (int q = 0; q < NQ; ++q) {
+        qv[q] = ediv_prepared(a[q], p);
+        estore(Q + ((long long)c * m + q * NT + tid) * es, qv[q]);
+      }
       fence_proxy_async();
+      if constexpr (PAIR) {
+        if (rank == 0) {  // push q_c to the partner, which pivots c+1 next
+          if (!wait_cluster_bar(&bar[5], ph5)) return false;
+          ph5 ^= 1;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            st_async_elem<E>(peer_qd + (uint32_t)((q * NT + tid) * es * sizeof(double)), qv[q], peer_b4);
+        }
+      }
       publish(ready, c);
     }
     return true;
@@ -994,7 +1099,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
     E a[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) a[q] = eload<E>(A + ((long long)q * NT + tid) * es);
-    if (!pivot(0, a)) return;
+    if (!pivot(0, a)) {
+      leave();
+      return;
+    }
   }
   auto first_after = [&](int k) { return k + 1 + (((cta - (k + 1)) % G) + G) % G; };
   // No proxy fence at the issue: every generic write of A and Q is followed
@@ -1045,12 +1153,29 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
   for (int k = 0; k < n; ++k) {
     const int j0 = first_after(k);
     if (j0 > n) break;
-    if ((late & 2) ? !wait_pivot(ready, k, status) : !wait1(k)) return;
-    if (QB == 2) qs = k & 1;
-    if (tid == 0 && qpre != k) issue_q(k, qs);
-    mbar_wait(&bar[2 + qs], ph[2 + qs]);
-    ph[2 + qs] ^= 1;
-    const E *qb = qbuf + (size_t)qs * m;
+    // PAIR: rank 1's pivot sweep takes q_k from its partner's push
+    const bool pair = PAIR && rank == 1 && j0 == k + 1;
+    const E *qb;
+    if (pair) {
+      if (tid == 0) mbar_expect_tx(&bar[4], cbytes);
+      const bool ok = wait_cluster_bar(&bar[4], ph4);
+      ph4 ^= 1;
+      if (!ok) {
+        leave();
+        return;
+      }
+      qb = qd;
+    } else {
+      if ((late & 2) ? !wait_pivot(ready, k, status) : !wait1(k)) {
+        leave();
+        return;
+      }
+      if (QB == 2) qs = k & 1;
+      if (tid == 0 && qpre != k) issue_q(k, qs);
+      mbar_wait(&bar[2 + qs], ph[2 + qs]);
+      ph[2 + qs] ^= 1;
+      qb = qbuf + (size_t)qs * m;
+    }
     for (int j = j0; j <= n; j += G) {
       int jn = j + G;
       if (jn > n) jn = k + 1 < n ? first_after(k + 1) : n + 1;
@@ -1095,7 +1220,10 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
       }
       fence_proxy_async();
       if (tid == 0) estore(R + ((long long)j * (n + 1) + k) * es, r);
-      if (j == k + 1 && !pivot(k + 1, a)) return;
+      if (j == k + 1 && !pivot(k + 1, a)) {
+        leave();
+        return;
+      }
       if (!(late & 1)) __syncthreads();  // colb[s] and the reduction slots are free
       if (pf) {
         s ^= 1;
@@ -1104,7 +1232,14 @@ __global__ void __launch_bounds__(256, 2) k_mgs_pipe(double *__restrict__ A, int
         inbuf = (jn == j) ? j : -1;
       }
     }
+    if constexpr (PAIR) {
+      if (pair) {
+        __syncthreads();  // every thread is done with the pushed q_k
+        if (tid == 0) remote_arrive(peer_b5);
+      }
+    }
   }
+  leave();
 }
 
 // back substitution R x = y, y = R[:n, n] (mgs.py:229-247): descending j,
@@ -1339,8 +1474,63 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   return true;
 }
 
+// PAIR launch of k_mgs_pipe (complex/real double): clusters of two CTAs,
+// cooperative; false when the clusters cannot all be resident
+template <class E, int NQ>
+static bool pipe_launch_pair(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
+  MgsStatus *status = w.status.as<MgsStatus>();
+  double *orig = w.orig.d();
+  double eps = level_eps(Traits<E>::nc);
+  constexpr int QB = 1;
+  const size_t smem = (size_t)(2 + QB + 1) * m * Traits<E>::es * sizeof(double);
+  auto kern = k_mgs_pipe<E, NQ, QB, true>;
+  PN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PN_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  if (per_sm <= 0) return false;
+  int grid = std::min(per_sm * num_sms(), n + 1) & ~1;  // even: whole clusters, G even
+  if (grid < 2) return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, (const void *)kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (2 * nclusters < grid) grid = 2 * nclusters;
+  if (grid < 2) return false;
+  cfg.gridDim = dim3(grid);
+  cfg.numAttrs = 2;
+  w.ready.ensure((size_t)(n + 1) * sizeof(int));
+  PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
+  int *ready = w.ready.as<int>();
+  int late = 0;
+  unsigned long long *tr = nullptr;
+  trace_begin(n, &tr);
+  PN_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, A, m, n, orig, eps, Q, R, status, ready, late));
+  trace_end(n, tr, st);
+  count_launch(1);
+  return true;
+}
+
 template <class E, int NQ>
 static bool pipe_launch(int m, int n, double *A, double *Q, double *R, MgsWork &w, cudaStream_t st) {
+  if constexpr (Traits<E>::nc == 1) {
+    const char *pv = getenv("PN_PIPE_PAIR");
+    if (pv && atoi(pv) == 1 && pipe_launch_pair<E, NQ>(m, n, A, Q, R, w, st)) return true;
+  }
   MgsStatus *status = w.status.as<MgsStatus>();
   double *orig = w.orig.d();
   const double eps = level_eps(Traits<E>::nc);

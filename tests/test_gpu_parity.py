@@ -186,14 +186,18 @@ def test_evaluate_reference_objects(gpu):
 
 # -- least squares -----------------------------------------------------------------------
 
-@pytest.fixture(params=["flow", "dataflow", "sweeps", "pipe/late0", "pipe/late1", "small"])
+@pytest.fixture(params=["flow", "dataflow", "sweeps", "pipe/late0", "pipe/late1", "pipe/pair", "small"])
 def mgs_mode(request, monkeypatch):
     """Every MGS schedule (priority flow, dataflow, launch per sweep, TMA pipe
-    with the prefetch before the reduction or after its first barrier, one CTA)."""
-    mode, _, late = request.param.partition("/late")
+    with the prefetch before the reduction or after its first barrier, the
+    pipe on 2-CTA clusters with q pushed through distributed shared memory
+    (d), one CTA)."""
+    mode, _, opt = request.param.partition("/")
     monkeypatch.setenv("PN_MGS_MODE", mode)
-    if late:
-        monkeypatch.setenv("PN_PIPE_LATE", late)
+    if opt.startswith("late"):
+        monkeypatch.setenv("PN_PIPE_LATE", opt[4:])
+    if opt == "pair":
+        monkeypatch.setenv("PN_PIPE_PAIR", "1")
     return mode
 
 
