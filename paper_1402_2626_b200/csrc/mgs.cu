@@ -212,15 +212,28 @@ __device__ __forceinline__ void load_rows_cg(E (&v)[B], const double *__restrict
 // publishes x_j in shared memory and then the step count with a block-scope
 // release store; the lookahead group spins on an acquire load (libcu++
 // atomic_ref, so the ordering is explicit to the compiler and the tools).
-__device__ __forceinline__ void step_publish(int *step, int v) {
-  cuda::atomic_ref<int, cuda::thread_scope_block>(*step).store(v, cuda::memory_order_release);
+// Step hand-off of the back-substitution kernels: one mbarrier per step slot
+// of a 32-row block (count 1: the thread that stores x_j arrives with release
+// semantics; the lookahead group waits on the slot's phase with acquire).
+// Only blocks with a lookahead group (b > 0) arrive, so every completed phase
+// has its waiter; slot s has completed one phase per earlier block that used
+// it (the first block, processed first, is the short one: n0 rows), so block
+// number p (in processing order) waits for parity (p - (s >= n0)) & 1.  An
+// mbarrier is a synchronisation object the sanitizers track, unlike an atomic
+// counter.
+__device__ __forceinline__ void xslot_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-__device__ __forceinline__ void step_wait(int *step, int above) {
-  cuda::atomic_ref<int, cuda::thread_scope_block> a(*step);
-  while (a.load(cuda::memory_order_acquire) <= above) __nanosleep(20);
-}
-__device__ __forceinline__ void step_reset(int *step) {
-  cuda::atomic_ref<int, cuda::thread_scope_block>(*step).store(0, cuda::memory_order_relaxed);
+__device__ __forceinline__ uint32_t xslot_parity(int p, int s, int n0) { return (uint32_t)(p - (s >= n0 ? 1 : 0)) & 1; }
+__device__ __forceinline__ void xslot_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
 }
 
 // publish pivot k: make this CTA's Q/R writes visible, then raise the flag
@@ -1854,10 +1867,10 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
   E *sX = sV + 32 * 32;                     // [2][32]: x of block b at parity b & 1
   E *sY = sX + 64;                          // block b-1 rows after the lookahead
   RDiv<NC> *sP = reinterpret_cast<RDiv<NC> *>(sY + 32);
-  __shared__ int s_step[1];  // solver steps whose x_j is in sX
+  __shared__ __align__(8) uint64_t s_xbar[32];  // x_j of step s of a block is in sX
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;
-  if (threadIdx.x == 0) step_reset(s_step);
+  if (blockIdx.x == 0 && threadIdx.x < 32) mbar_init(&s_xbar[threadIdx.x], 1);  // only CTA 0 hands off
   const long long ld = n + 1;
   const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
   for (int j = gtid; j < n; j += gsize) {
@@ -1919,16 +1932,17 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
         ++q;
       };
       __syncthreads();  // sY was read before the lookahead group rewrites it
+      const int pblk = nb - 1 - b, n0 = n - 32 * (nb - 1);  // processing index; rows of the first block
       if (solver) {
         // the solver's steps sync on a named barrier of its 128 threads; the
-        // lookahead group follows the published-step counter instead
+        // lookahead group follows the step slots instead
         for (int s = 0; s < nbk; ++s) {
           const int jl = nbk - 1 - s;
           if ((jl >> 3) == (tt >> 5)) {
             const E xj = lp_div(yr, sD[jl * 32 + jl], sP[jl], p, g4);
             if (rl == jl && p == 0) {
               sX[par * 32 + jl] = xj;
-              step_publish(s_step, s + 1);
+              if (b > 0) xslot_arrive(&s_xbar[s]);  // block 0 has no lookahead group
             }
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1941,13 +1955,12 @@ __global__ void __launch_bounds__(256) k_backsub_look(const double *__restrict__
         // block b+1's x first, then block b's as the solver publishes them
         while (q < ncu) look();
         for (int s = 0; s < nbk; ++s) {
-          step_wait(s_step, s);
+          xslot_wait(&s_xbar[s], xslot_parity(pblk, s, n0));
           look();
         }
         if (p == 0) sY[rl] = v;
       }
       __syncthreads();
-      if (t == 0) step_reset(s_step);
       if (solver && tt < nbk) estore(x + (long long)(lo + tt) * es, sX[par * 32 + tt]);
     } else if (b + 1 < nb) {
       // rows below block b-1 take block b+1's x (descending columns)
@@ -1987,10 +2000,10 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
   E *sX = sV + 32 * 32;                     // [2][32]
   E *sY = sX + 64;                          // block b-1 rows after the lookahead
   RD *sP = reinterpret_cast<RD *>(sY + 32);
-  __shared__ int s_step[1];
+  __shared__ __align__(8) uint64_t s_xbar[32];  // x_j of step s of a block is in sX
   cg::grid_group grid = cg::this_grid();
   if (status->code) return;
-  if (threadIdx.x == 0) step_reset(s_step);
+  if (blockIdx.x == 0 && threadIdx.x < 32) mbar_init(&s_xbar[threadIdx.x], 1);  // only CTA 0 hands off
   const long long ld = n + 1;
   const int gtid = blockIdx.x * NT + threadIdx.x, gsize = gridDim.x * NT;
   for (int j = gtid; j < n; j += gsize) {
@@ -2026,6 +2039,7 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
       }
       if (threadIdx.x < nbk) sP[threadIdx.x] = prep[lo + threadIdx.x];
       __syncthreads();
+      const int pblk = nb - 1 - b, n0 = n - 32 * (nb - 1);  // processing index; rows of the first block
       if (warp == 0) {
         E yr = ezero<E>();
         if (lane < nbk) yr = b == nb - 1 ? eload<E>(y + (long long)(lo + lane) * es) : sY[lane];
@@ -2036,7 +2050,7 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
           if (lane == jl) {
             xl = ediv_with(yr, sD[jl * 32 + jl], sP[jl]);
             sX[par * 32 + jl] = xl;
-            step_publish(s_step, s + 1);
+            if (b > 0) xslot_arrive(&s_xbar[s]);  // block 0 has no lookahead warp
           }
           const E xj = eshfl_idx(xl, jl);
           if (lane < jl) yr = esub(yr, emul(sD[jl * 32 + lane], xj));
@@ -2047,13 +2061,12 @@ __global__ void __launch_bounds__(NT) k_backsub_blocked_look(const double *__res
         for (int jj = ncu - 1; jj >= 0; --jj) v = esub(v, emul(sV[jj * 32 + lane], sX[(par ^ 1) * 32 + jj]));
         for (int s = 0; s < nbk; ++s) {
           const int jl = nbk - 1 - s;
-          step_wait(s_step, s);
+          xslot_wait(&s_xbar[s], xslot_parity(pblk, s, n0));
           v = esub(v, emul(sU[jl * 32 + lane], sX[par * 32 + jl]));
         }
         sY[lane] = v;
       }
       __syncthreads();
-      if (threadIdx.x == 0) step_reset(s_step);
     } else if (b + 1 < nb) {
       const int c0 = lo + 32, nc1 = min(n, lo + 64) - c0;
       for (int r = gtid - NT; r < lo - 32; r += gsize - NT) {

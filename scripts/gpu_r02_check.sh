@@ -12,7 +12,7 @@ $S --tool memcheck python -m pytest tests/test_eval_rows.py -q -p no:cacheprovid
 echo "rc=$?" >> gpurun_out/${T}_memcheck_rows.log
 $S --tool racecheck python -m pytest tests/test_eval_rows.py -q -p no:cacheprovider -x -k "every_tree_base or ragged" > gpurun_out/${T}_racecheck_rows.log 2>&1
 echo "rc=$?" >> gpurun_out/${T}_racecheck_rows.log
-$S --tool synccheck python -m pytest tests/test_eval_rows.py -q -p no:cacheprovider -x -k "every_tree_base" > gpurun_out/${T}_synccheck_rows.log 2>&1
+$S --tool synccheck --num-cuda-barriers 64 python -m pytest tests/test_eval_rows.py -q -p no:cacheprovider -x -k "every_tree_base" > gpurun_out/${T}_synccheck_rows.log 2>&1
 echo "rc=$?" >> gpurun_out/${T}_synccheck_rows.log
 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
 tail -2 gpurun_out/${T}_tests.log
