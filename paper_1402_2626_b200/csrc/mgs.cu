@@ -1450,10 +1450,12 @@ static bool flow_launch(int m, int n, double *A, double *Q, double *R, MgsWork &
   PN_CHECK_CUDA(cudaMemsetAsync(w.ready.p, 0, (size_t)(n + 1) * sizeof(int), st));
   int *ready = w.ready.as<int>();
   // hold: a CTA whose critical column pivots within `hold` sweeps of the
-  // pivot in flight does no lagging work (PN_FLOW_HOLD, 0 = off; 1 measured
-  // 129.5 -> 124.2 ms per cqd step, 2 and 3 within noise of 1)
+  // pivot in flight does no lagging work (PN_FLOW_HOLD, 0 = off; round 1: 1
+  // measured 129.5 -> 124.2 ms per cqd step; round 2, final kernels: cqd
+  // factorisation 111.8 / 102.70 / 102.40 / 102.42 / 102.43 ms for hold =
+  // 0 / 1 / 2 / 3 / 4, profiles/r02/exp ab60/ab61)
   const char *hv = getenv("PN_FLOW_HOLD");
-  int hold = hv ? atoi(hv) : 1;
+  int hold = hv ? atoi(hv) : 2;
   const char *lv = getenv("PN_FLOW_LAG");
   int lag = lv ? atoi(lv) : 1 << 30;
   flow_owner_table(n, grid, w, st);
