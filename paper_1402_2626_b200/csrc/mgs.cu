@@ -1718,6 +1718,15 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     if constexpr (B == 8) {
       if (m <= 1536 && flow_launch<E, B, 192>(m, n, A, Q, R, w, st)) return;
     }
+    // qd with 3/4 of the CTA's rows used (256 < m <= 384, 512 < m <= 768):
+    // 192-thread CTAs instead of 256 with a quarter of the threads idle --
+    // cqd factorisation at 768 rows 71.4 -> 61.0 ms (profiles/r02/exp ab62).
+    // PN_FLOW_192=0 keeps 256 threads.
+    if constexpr ((B == 4 || B == 2) && Traits<E>::nc == 4) {
+      const char *f3 = getenv("PN_FLOW_192");
+      if (!(f3 && atoi(f3) == 0) && m > 128 * B && m <= 192 * B && flow_launch<E, B, 192>(m, n, A, Q, R, w, st))
+        return;
+    }
     // real qd, 2048 < m <= 4096 (Chandrasekhar real qd): the column fills
     // one CTA's shared memory either way; 16 warps x 8 rows instead of 8 x 16
     // (PN_FLOW_WIDE=0 keeps the 256-thread CTA)

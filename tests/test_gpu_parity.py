@@ -229,7 +229,7 @@ def test_breakdown_golden(gpu, mgs_mode):
 
 @pytest.mark.parametrize("lv,m,n", [("cqd", 160, 128), ("cdd", 513, 200), ("rdd", 1030, 64), ("cd", 256, 256),
                                     ("cdd", 768, 300), ("rd", 512, 512), ("cdd", 1024, 160), ("rdd", 512, 200),
-                                    ("cdd", 256, 100)])
+                                    ("cdd", 256, 100), ("cqd", 700, 90), ("rqd", 768, 64), ("cqd", 300, 120)])
 def test_least_squares_vs_oracle(gpu, mgs_mode, lv, m, n):
     from paper_1402_2626_b200.mgs import AugmentedMatrix, least_squares_solve
     from paper_1402_2626_b200.varith import VecContext
