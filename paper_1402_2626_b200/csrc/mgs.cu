@@ -1733,6 +1733,11 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     if constexpr (B == 16 && Traits<E>::nc == 4 && !Traits<E>::cplx) {
       const char *fw = getenv("PN_FLOW_WIDE");
       const bool wide = fw ? strcmp(fw, "0") != 0 : true;
+      // up to 3072 rows: 384 threads x 8 rows fill the CTA (Chandrasekhar
+      // real qd n = 3048: 5.75 -> 5.59 s; PN_FLOW_384=0 keeps 512)
+      const char *f3 = getenv("PN_FLOW_384");
+      if (wide && m > 2048 && m <= 3072 && !(f3 && atoi(f3) == 0) && flow_launch<E, 8, 384>(m, n, A, Q, R, w, st))
+        return;
       if (wide && m > 2048 && flow_launch<E, 8, 512>(m, n, A, Q, R, w, st)) return;
     }
     if (flow_launch<E, B, kMgsThreads>(m, n, A, Q, R, w, st)) return;
@@ -1749,6 +1754,10 @@ static void mgs_run(int m, int n, double *A, double *Q, double *R, MgsWork &w, c
     const char *fw = getenv("PN_FLOW_WIDE");
     const int wide = fw ? atoi(fw) : (m > 2048 ? (Traits<E>::nc == 2 && Traits<E>::cplx ? 2 : 1) : 0);
     if constexpr (B == 16 && Traits<E>::nc == 2) {
+      // up to 3072 rows: 384 threads x 8 rows (Chandrasekhar cdd n = 3072:
+      // 2.50 -> 2.45 s; PN_FLOW_384=0 keeps 512)
+      const char *f3 = getenv("PN_FLOW_384");
+      if (wide == 2 && m <= 3072 && !(f3 && atoi(f3) == 0) && flow_launch<E, 8, 384>(m, n, A, Q, R, w, st)) return;
       if (wide == 2 && flow_launch<E, 8, 512>(m, n, A, Q, R, w, st)) return;
     }
     if (wide && flow_launch<E, 4, 1024>(m, n, A, Q, R, w, st)) return;

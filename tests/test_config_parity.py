@@ -252,7 +252,7 @@ def test_cyclic_300_all_large_buckets_vs_oracle(gpu, monkeypatch, lv, warp):
 
 
 @pytest.mark.parametrize("lv,m,n", [("cdd", 4096, 48), ("cd", 3000, 200), ("rdd", 2100, 130), ("rqd", 4064, 40),
-                                    ("rqd", 2100, 90)])
+                                    ("rqd", 2100, 90), ("cdd", 2500, 60), ("rqd", 3048, 50)])
 @pytest.mark.parametrize("wide", ["2", "1", "0"])
 def test_tall_least_squares_wide_flow_vs_oracle(gpu, monkeypatch, lv, m, n, wide):
     """1024 < m <= 4096 rows: d/dd take the 512-thread (dd) or 1024-thread
